@@ -498,3 +498,20 @@ def test_dt_auto(oracle_lib):
     V = np.array([1500.0, 4500.0, 3000.0], np.float32)
     assert oracle.dt_auto(10.0, V) == np.float32(0.4 * 10.0 / 4500.0)
     assert oracle.dt_auto((10.0, 5.0, 20.0), V) == np.float32(0.4 * 5.0 / 4500.0)
+
+
+def test_source_location_and_scaling_asymmetric(oracle_lib):
+    # From the zero state, one step leaves exactly fp32((V(src) dt)^2 w[0]) at the
+    # (i, j, k) source cell and zero elsewhere; an asymmetric source and a random
+    # V pin the index order of the source cell and of the V lookup (PAPER.md L238
+    # Eq. 2 RHS dt^2 V^2 f).
+    s = synth.scenario("RAGGED")
+    g = oracle.make_geom(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    V = synth.velocity(s)
+    i, j, k = 29, 17, 33
+    u, _, st, _ = oracle.propagate(g, V, np.array([0.75], np.float32), 1, (i, j, k),
+                                   dtype=np.float64, round32=False)
+    exp = (float(V[k, j, i]) * float(s.dt32)) ** 2 * 0.75
+    assert u[k, j, i] == pytest.approx(exp, rel=1e-15)
+    u[k, j, i] = 0
+    assert not u.any()
