@@ -1,0 +1,253 @@
+/* wave.h -- C ABI of the B200-native 25-point acoustic wave stepper
+ * (arXiv 2009.04619, "Accelerating High-Order Stencils on GPUs").
+ *
+ * The calls follow the paper's problem statement (PAPER.md L255-267,
+ * Algorithm 1: data f, result u^n for n = 1..T; L300-301: inner size and PML
+ * width are inputs of a simulation): create an nx*ny*nz grid with spacing, dt
+ * and a velocity model, inject a source wavelet, step N times, read back the
+ * wavefield.  One step computes, at every point of the extended domain,
+ *
+ *   inner (Eq. 2-3):
+ *     u_next = 2u - u_prev + (V dt)^2 Lap8(u)
+ *   PML   (25-pt on u + 7-pt star on eta;
+ *          formula SPEC.md L152; profile DESIGN.md R2/R3):
+ *     u_next = [2u - (1 - eta dt) u_prev + (V dt)^2 (Lap8(u) + grad eta . grad u)]
+ *              / (1 + eta dt),   eta = eta_max (d/w)^2, d = Chebyshev distance
+ *   then the source (Alg. 1, Eq. 2 RHS):
+ *     u_next[src] += fp32((V_src dt)^2 * w[n])
+ *
+ * in fp32 with every constant computed in fp64 and rounded once (R8).
+ *
+ * Conventions for every call:
+ *  - Pointers: "device" = CUDA device memory of the current device, "host" =
+ *    any host memory (pinned memory makes copies asynchronous).  `where`
+ *    arguments say which.  `stream` is a cudaStream_t passed as void*; NULL =
+ *    the legacy default stream.  All device work is enqueued on `stream`;
+ *    calls return before it completes unless stated otherwise.
+ *  - Errors: every call returns a wave_status; no exception crosses the ABI.
+ *    wave_last_error() returns a thread-local message for the last failure.
+ *    Configuration errors are detected before anything is written.
+ *    Asynchronous CUDA faults surface at the next synchronising call
+ *    (wave_read to host, wave_check_finite) as WAVE_ERR_CUDA.
+ *  - Ownership: the caller owns the big device buffers (two wavefield
+ *    buffers and the vdt2 buffer, sized by wave_layout), the streams and any
+ *    process group.  The plan owns its small device tables, the source
+ *    increments, the TMA descriptors, its CUDA graphs and the step counter.
+ *    Bound buffers must outlive all enqueued work.  A plan is not
+ *    thread-safe; different plans are independent.
+ */
+#ifndef WAVE25_WAVE_H
+#define WAVE25_WAVE_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define WAVE_API __attribute__((visibility("default")))
+#else
+#define WAVE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; 0..3 mirror SPEC.md L585 exit codes. */
+typedef enum {
+    WAVE_OK = 0,
+    WAVE_ERR_CONFIG = 1,     /* invalid descriptor / argument, nothing written */
+    WAVE_ERR_UNSTABLE = 2,   /* non-finite wavefield        */
+    WAVE_ERR_VERIFY = 3,     /* reserved for verification harnesses           */
+    WAVE_ERR_CUDA = 4,       /* CUDA runtime / driver error                    */
+    WAVE_ERR_ALLOC = 5,      /* host or device allocation failure              */
+    WAVE_ERR_STATE = 6       /* call out of order (e.g. step before bind)       */
+} wave_status;
+
+typedef enum { WAVE_MEM_HOST = 0, WAVE_MEM_DEVICE = 1 } wave_mem;
+
+/* Kernel family used by wave_step.  STREAM (default) is the production
+ * path: TMA-fed z-streaming interior kernel + PML wall kernels + source
+ * kernel.  NAIVE is one thread per point with all 25 loads from global memory
+ * (the paper's gmem code shape), kept as an ablation /
+ * debugging path; both compute bitwise-identical values. */
+typedef enum { WAVE_KERNEL_STREAM = 0, WAVE_KERNEL_NAIVE = 1 } wave_kernel;
+
+/* Problem descriptor.
+ *  nx, ny, nz  extended domain (inner + PML on every face) of
+ *              THIS plan; x innermost.  nz = planes of this rank's z-slab
+ *              (= nz_global on one GPU).                         all >= 1
+ *  pml_width   w, uniform on all six faces;
+ *              0 <= 2w < min(nx, ny, nz_global)
+ *  kernel      wave_kernel
+ *  hx, hy, hz  spacing (m), > 0 (per-axis, R1)
+ *  dt          time step (s) as the fp32 value used; > 0, or 0 = automatic
+ *              fp32(0.4 h_min / Vmax) resolved at wave_set_velocity (SPEC.md
+ *              L199; single-slab plans only).  Rejected above the Courant
+ *              limit dt Vmax sqrt(sum_a 1/h_a^2) <= 2/sqrt(6.5016...)
+ *  eta_max     PML damping maximum (1/s), >= 0.  Default 4 (stable; SPEC's
+ *              100 diverges, R5)
+ *  nz_global,  this slab covers global planes [z_offset, z_offset + nz) of
+ *  z_offset    nz_global; (nz_global, z_offset) = (nz, 0) on one GPU
+ */
+typedef struct {
+    int64_t nx, ny, nz;
+    int32_t pml_width;
+    int32_t kernel;
+    double hx, hy, hz;
+    float dt;
+    float reserved0;
+    double eta_max;
+    int64_t nz_global, z_offset;
+} wave_desc;
+
+/* Device memory layout the caller must allocate (wave_layout).
+ * Wavefield buffer: [planes][ny][pitch_x] fp32, planes = nz + 2*ghost_z;
+ * element (i, j, k) (local k) lives at ((k + ghost_z)*ny + j)*pitch_x + i.
+ * The ghost_z = 4 planes on each z side are the zero Dirichlet fringe
+ * at the global ends and the neighbour's planes (halo) between
+ * slabs.  x/y have no stored fringe (TMA out-of-bounds fill supplies zeros).
+ * vdt2 buffer: [nz][ny][pitch_x] fp32 holding fp32((V dt)^2).
+ * Base addresses must be aligned to align_bytes. */
+typedef struct {
+    int64_t pitch_x;      /* floats per row: >= nx, multiple of 4 (16 B TMA stride rule) */
+    int64_t ghost_z;      /* 4 = stencil radius R                     */
+    int64_t planes;       /* nz + 2*ghost_z                                               */
+    int64_t elems_u;      /* floats per wavefield buffer                                  */
+    int64_t elems_vdt2;   /* floats in the vdt2 buffer                                    */
+    int64_t align_bytes;  /* 128                                                          */
+} wave_layout_info;
+
+/* One region of the paper's 7-region decomposition (PAPER.md L342-356,
+ * Fig. 1; SPEC.md L239-247 axis binding: top/bottom split z, front/back
+ * split y, left/right split x). Global coordinates. */
+typedef enum {
+    WAVE_REGION_INNER = 0, WAVE_REGION_TOP = 1, WAVE_REGION_BOTTOM = 2,
+    WAVE_REGION_FRONT = 3, WAVE_REGION_BACK = 4, WAVE_REGION_LEFT = 5, WAVE_REGION_RIGHT = 6
+} wave_region_kind;
+
+typedef struct {
+    int32_t kind;
+    int32_t reserved0;
+    int64_t lo[3];        /* x, y, z origin */
+    int64_t ext[3];       /* extents (>= 0)  */
+} wave_region;
+
+typedef struct wave_plan wave_plan;   /* opaque */
+
+/* ---- host-only calls (no GPU needed) ------------------------------------ */
+
+/* Library version string, e.g. "wave25 0.1.0 sm_100a". Never fails. */
+WAVE_API const char *wave_version(void);
+
+/* Thread-local text of the last failure on this thread ("" if none). */
+WAVE_API const char *wave_last_error(void);
+
+/* Validate `desc` (all CONFIG rules except the velocity-dependent Courant
+ * check) and return the buffer sizes to allocate in *out. */
+WAVE_API wave_status wave_layout(const wave_desc *desc, wave_layout_info *out);
+
+/* The 7 regions (inner, top, bottom, front, back, left, right) of the GLOBAL
+ * extended domain nx*ny*nz_global.  out must hold 7. */
+WAVE_API wave_status wave_decompose(const wave_desc *desc, wave_region *out);
+
+/* fp32 constants the plan uses, computed in fp64 and rounded once:
+ * c13 = {c_xyz, c_x1..4, c_y1..4, c_z1..4},
+ * eta/A/B[w+1] = eta_max (d/w)^2, 1 - eta dt, 1 + eta dt (SPEC.md L152,
+ * DESIGN.md R2), inv2h[3] = 1/(2 h_a).  Uses desc->dt (must be > 0).
+ * Any output pointer may be NULL.  Host memory. */
+WAVE_API wave_status wave_constants(const wave_desc *desc, float *c13, float *eta, float *A,
+                           float *B, float *inv2h);
+
+/* ---- plan lifecycle ------------------------------------------------------ */
+
+/* Validate desc and create a plan on the current CUDA device. */
+WAVE_API wave_status wave_plan_create(const wave_desc *desc, wave_plan **out);
+
+/* Bind caller-owned DEVICE buffers (sizes from wave_layout).  Zero-fills both
+ * wavefield buffers (u^0 = u^{-1} = 0) and the vdt2 buffer,
+ * builds TMA descriptors, resets the step counter to 0. */
+WAVE_API wave_status wave_plan_bind(wave_plan *plan, float *u0, float *u1, float *vdt2, void *stream);
+
+/* Destroy the plan (caller synchronises its streams first). NULL is a no-op. */
+WAVE_API void wave_plan_destroy(wave_plan *plan);
+
+/* ---- inputs -------------------------------------------------------------- */
+
+/* Velocity model V (m/s), dense [nz][ny][nx] fp32 of THIS slab, all > 0
+ * (SPEC.md L118), in `where` memory.  Computes vdt2 = fp32((V dt)^2) on the
+ * device.  If desc.dt == 0 resolves dt = fp32(0.4 h_min / Vmax) first (reads
+ * V back; synchronises `stream`).  Performs the Courant check (CONFIG).
+ * If a source was set, its increments are rebuilt. */
+WAVE_API wave_status wave_set_velocity(wave_plan *plan, const float *vel, int32_t where, void *stream);
+
+/* Point source at GLOBAL cell (i, j, k), strictly inside the inner region
+ * (SPEC.md L114), with wavelet samples w[0..nsamples) (host fp32, copied);
+ * step n injects fp32(vdt2[src] * w[n]) (0 for n >= nsamples).  On a slab
+ * that does not own plane k the call only records the source.  Requires
+ * wave_set_velocity first. */
+WAVE_API wave_status wave_set_source(wave_plan *plan, int64_t i, int64_t j, int64_t k,
+                            const float *wavelet, int64_t nsamples, void *stream);
+
+/* Optional initial state: u^{-1} (uprev) and u^0 (ucur), dense [nz][ny][nx]
+ * fp32 in `where` memory (either may be NULL = zero).  Resets the step
+ * counter to 0 and clears the halo planes. */
+WAVE_API wave_status wave_set_state(wave_plan *plan, const float *uprev, const float *ucur,
+                           int32_t where, void *stream);
+
+/* ---- stepping ------------------------------------------------------------ */
+
+/* Advance nsteps >= 0 time steps (Algorithm 1 lines 1-5 per step).  Single-
+ * slab plans only (multi-slab plans use the split calls below).  Steps are
+ * replayed from CUDA graphs captured on first use. */
+WAVE_API wave_status wave_step(wave_plan *plan, int64_t nsteps, void *stream);
+
+/* Split step for z-slab decomposition (one step = edges, halo exchange by the
+ * caller, interior, finish; any order of edges/interior, same values as
+ * wave_step):
+ *  edges    : compute u_next on local planes [0, 4) and [nz-4, nz) (+ source
+ *             if it lies there) -- the planes the neighbours need
+ *  interior : compute u_next on local planes [4, nz-4) (+ source if there)
+ *  finish   : role swap and step counter (host-side bookkeeping only) */
+WAVE_API wave_status wave_step_edges(wave_plan *plan, void *stream);
+WAVE_API wave_status wave_step_interior(wave_plan *plan, void *stream);
+WAVE_API wave_status wave_step_finish(wave_plan *plan);
+
+/* Device pointers, into the buffer that wave_step_edges writes (the next
+ * u^n), of the 4-plane blocks to SEND to the lower / upper neighbour (local
+ * planes [0,4) and [nz-4,nz)) and of the ghost blocks to RECEIVE into (the 4
+ * planes below / above the slab).  Each block is *count contiguous floats.
+ * Valid between wave_step_edges and wave_step_finish. */
+WAVE_API wave_status wave_halo_views(const wave_plan *plan, float **send_lo, float **send_hi,
+                            float **recv_lo, float **recv_hi, int64_t *count);
+
+/* ---- outputs ------------------------------------------------------------- */
+
+/* Copy u^n (which = 0) or u^{n-1} (which = 1) to dst, dense [nz][ny][nx] fp32
+ * in `where` memory.  A host destination synchronises `stream` and reports
+ * pending asynchronous CUDA errors. */
+WAVE_API wave_status wave_read(const wave_plan *plan, int32_t which, float *dst, int32_t where,
+                      void *stream);
+
+/* Device pointer to the first element (i,j,k) = (0,0,0) of u^n (which = 0) or
+ * u^{n-1} (which = 1) inside its padded buffer; row pitch = pitch_x, plane
+ * pitch = ny*pitch_x.  Zero-copy view; valid until the next step. */
+WAVE_API wave_status wave_field_ptr(const wave_plan *plan, int32_t which, float **out);
+
+/* max |u^n| into *h_maxabs (host); synchronises `stream`.  Returns
+ * WAVE_ERR_UNSTABLE (with the step number in wave_last_error) when any value
+ * is non-finite. */
+WAVE_API wave_status wave_check_finite(wave_plan *plan, float *h_maxabs, void *stream);
+
+/* Number of completed steps n (u^n is current). -1 on NULL. */
+WAVE_API int64_t wave_step_index(const wave_plan *plan);
+
+/* The dt in use (after auto resolution), 0 if unresolved or NULL. */
+WAVE_API float wave_get_dt(const wave_plan *plan);
+
+/* Number of kernel launches one wave_step(plan, 1) enqueues (for launch
+ * accounting in benchmarks); -1 on NULL. */
+WAVE_API int32_t wave_launches_per_step(const wave_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WAVE25_WAVE_H */

@@ -1,0 +1,226 @@
+"""ctypes binding of include/wave.h -- argument marshalling only.
+
+Every function here has the name of the C entry point it calls and does no
+arithmetic of the method: all of the time step runs in the CUDA kernels of
+libwave25.so.  There is no CPU fallback: if the library is missing, importing
+`lib()` raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libwave25.so")
+
+WAVE_OK, WAVE_ERR_CONFIG, WAVE_ERR_UNSTABLE, WAVE_ERR_VERIFY, WAVE_ERR_CUDA, WAVE_ERR_ALLOC, WAVE_ERR_STATE = range(7)
+STATUS_NAMES = {0: "WAVE_OK", 1: "WAVE_ERR_CONFIG", 2: "WAVE_ERR_UNSTABLE", 3: "WAVE_ERR_VERIFY",
+                4: "WAVE_ERR_CUDA", 5: "WAVE_ERR_ALLOC", 6: "WAVE_ERR_STATE"}
+WAVE_MEM_HOST, WAVE_MEM_DEVICE = 0, 1
+WAVE_KERNEL_STREAM, WAVE_KERNEL_NAIVE = 0, 1
+REGION_NAMES = ["inner", "top", "bottom", "front", "back", "left", "right"]
+
+EXPORTS = [
+    "wave_version", "wave_last_error", "wave_layout", "wave_decompose", "wave_constants",
+    "wave_plan_create", "wave_plan_bind", "wave_plan_destroy", "wave_set_velocity",
+    "wave_set_source", "wave_set_state", "wave_step", "wave_step_edges", "wave_step_interior",
+    "wave_step_finish", "wave_halo_views", "wave_read", "wave_field_ptr", "wave_check_finite",
+    "wave_step_index", "wave_get_dt", "wave_launches_per_step",
+]
+
+
+class WaveDesc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
+                ("pml_width", ctypes.c_int32), ("kernel", ctypes.c_int32),
+                ("hx", ctypes.c_double), ("hy", ctypes.c_double), ("hz", ctypes.c_double),
+                ("dt", ctypes.c_float), ("reserved0", ctypes.c_float),
+                ("eta_max", ctypes.c_double),
+                ("nz_global", ctypes.c_int64), ("z_offset", ctypes.c_int64)]
+
+
+class WaveLayout(ctypes.Structure):
+    _fields_ = [("pitch_x", ctypes.c_int64), ("ghost_z", ctypes.c_int64), ("planes", ctypes.c_int64),
+                ("elems_u", ctypes.c_int64), ("elems_vdt2", ctypes.c_int64), ("align_bytes", ctypes.c_int64)]
+
+
+class WaveRegion(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("lo", ctypes.c_int64 * 3), ("ext", ctypes.c_int64 * 3)]
+
+
+class WaveError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libwave25.so (build it with __graft_entry__.build()).  Raises if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: the CUDA library must be built "
+                                  "(python -c 'import __graft_entry__ as g; g.build()'); "
+                                  "there is no CPU fallback")
+            L = ctypes.CDLL(LIB_PATH)
+            P, i64, i32, f32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float
+            DP = ctypes.POINTER(WaveDesc)
+            sig = {
+                "wave_version": ([], ctypes.c_char_p),
+                "wave_last_error": ([], ctypes.c_char_p),
+                "wave_layout": ([DP, ctypes.POINTER(WaveLayout)], i32),
+                "wave_decompose": ([DP, ctypes.POINTER(WaveRegion)], i32),
+                "wave_constants": ([DP, P, P, P, P, P], i32),
+                "wave_plan_create": ([DP, ctypes.POINTER(P)], i32),
+                "wave_plan_bind": ([P, P, P, P, P], i32),
+                "wave_plan_destroy": ([P], None),
+                "wave_set_velocity": ([P, P, i32, P], i32),
+                "wave_set_source": ([P, i64, i64, i64, P, i64, P], i32),
+                "wave_set_state": ([P, P, P, i32, P], i32),
+                "wave_step": ([P, i64, P], i32),
+                "wave_step_edges": ([P, P], i32),
+                "wave_step_interior": ([P, P], i32),
+                "wave_step_finish": ([P], i32),
+                "wave_halo_views": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
+                                     ctypes.POINTER(P), ctypes.POINTER(i64)], i32),
+                "wave_read": ([P, i32, P, i32, P], i32),
+                "wave_field_ptr": ([P, i32, ctypes.POINTER(P)], i32),
+                "wave_check_finite": ([P, ctypes.POINTER(f32), P], i32),
+                "wave_step_index": ([P], i64),
+                "wave_get_dt": ([P], f32),
+                "wave_launches_per_step": ([P], i32),
+            }
+            for name, (args, res) in sig.items():
+                fn = getattr(L, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = L
+        return _lib
+
+
+def check(status: int) -> None:
+    if status != WAVE_OK:
+        raise WaveError(status, lib().wave_last_error().decode(errors="replace"))
+
+
+def make_desc(nx, ny, nz, pml_width, h, dt, eta_max=4.0, kernel=WAVE_KERNEL_STREAM,
+              nz_global=None, z_offset=0) -> WaveDesc:
+    hx, hy, hz = (h, h, h) if isinstance(h, (int, float)) else tuple(h)
+    return WaveDesc(int(nx), int(ny), int(nz), int(pml_width), int(kernel), float(hx), float(hy),
+                    float(hz), float(dt), 0.0, float(eta_max),
+                    int(nz if nz_global is None else nz_global), int(z_offset))
+
+
+# ---- thin wrappers, same names as the C ABI ------------------------------------------------
+
+def wave_version() -> str:
+    return lib().wave_version().decode()
+
+
+def wave_layout(desc: WaveDesc) -> WaveLayout:
+    out = WaveLayout()
+    check(lib().wave_layout(ctypes.byref(desc), ctypes.byref(out)))
+    return out
+
+
+def wave_decompose(desc: WaveDesc):
+    out = (WaveRegion * 7)()
+    check(lib().wave_decompose(ctypes.byref(desc), out))
+    return [dict(kind=REGION_NAMES[r.kind], lo=tuple(r.lo), ext=tuple(r.ext)) for r in out]
+
+
+def wave_constants(desc: WaveDesc) -> dict:
+    import numpy as np
+    w = desc.pml_width
+    c13 = np.zeros(13, np.float32)
+    eta, A, B = (np.zeros(w + 1, np.float32) for _ in range(3))
+    i2h = np.zeros(3, np.float32)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    check(lib().wave_constants(ctypes.byref(desc), p(c13), p(eta), p(A), p(B), p(i2h)))
+    return {"c_xyz": c13[0], "c_x": c13[1:5], "c_y": c13[5:9], "c_z": c13[9:13],
+            "eta": eta, "A": A, "B": B, "inv2h": i2h}
+
+
+def wave_plan_create(desc: WaveDesc) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    check(lib().wave_plan_create(ctypes.byref(desc), ctypes.byref(h)))
+    return h
+
+
+def wave_plan_bind(plan, u0: int, u1: int, vdt2: int, stream: int) -> None:
+    check(lib().wave_plan_bind(plan, u0, u1, vdt2, stream))
+
+
+def wave_plan_destroy(plan) -> None:
+    lib().wave_plan_destroy(plan)
+
+
+def wave_set_velocity(plan, vel_ptr: int, where: int, stream: int) -> None:
+    check(lib().wave_set_velocity(plan, vel_ptr, where, stream))
+
+
+def wave_set_source(plan, i, j, k, wavelet_ptr: int, nsamples: int, stream: int) -> None:
+    check(lib().wave_set_source(plan, int(i), int(j), int(k), wavelet_ptr, int(nsamples), stream))
+
+
+def wave_set_state(plan, uprev_ptr, ucur_ptr, where: int, stream: int) -> None:
+    check(lib().wave_set_state(plan, uprev_ptr, ucur_ptr, where, stream))
+
+
+def wave_step(plan, nsteps: int, stream: int) -> None:
+    check(lib().wave_step(plan, int(nsteps), stream))
+
+
+def wave_step_edges(plan, stream: int) -> None:
+    check(lib().wave_step_edges(plan, stream))
+
+
+def wave_step_interior(plan, stream: int) -> None:
+    check(lib().wave_step_interior(plan, stream))
+
+
+def wave_step_finish(plan) -> None:
+    check(lib().wave_step_finish(plan))
+
+
+def wave_halo_views(plan):
+    a, b, c, d = (ctypes.c_void_p() for _ in range(4))
+    n = ctypes.c_int64()
+    check(lib().wave_halo_views(plan, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                                ctypes.byref(d), ctypes.byref(n)))
+    return a.value, b.value, c.value, d.value, n.value
+
+
+def wave_read(plan, which: int, dst_ptr: int, where: int, stream: int) -> None:
+    check(lib().wave_read(plan, int(which), dst_ptr, where, stream))
+
+
+def wave_field_ptr(plan, which: int) -> int:
+    out = ctypes.c_void_p()
+    check(lib().wave_field_ptr(plan, int(which), ctypes.byref(out)))
+    return out.value
+
+
+def wave_check_finite(plan, stream: int) -> float:
+    v = ctypes.c_float()
+    check(lib().wave_check_finite(plan, ctypes.byref(v), stream))
+    return v.value
+
+
+def wave_step_index(plan) -> int:
+    return int(lib().wave_step_index(plan))
+
+
+def wave_get_dt(plan) -> float:
+    return float(lib().wave_get_dt(plan))
+
+
+def wave_launches_per_step(plan) -> int:
+    return int(lib().wave_launches_per_step(plan))

@@ -1,0 +1,142 @@
+// common.cuh -- device helpers shared by every kernel of the CUDA path:
+// mbarrier / TMA PTX wrappers for sm_100a and the per-point arithmetic of one
+// time step.  GPU side only; shares nothing with oracle/.
+//
+// The per-point functions are written with explicit __f*_rn intrinsics so
+// that nvcc's FMA contraction cannot differ between inline sites: every
+// kernel (naive, interior stream, wall stream, edges/interior split) produces
+// bitwise-identical values for the same point, which the 1-GPU == N-slab
+// bitwise test relies on.
+#pragma once
+#include <cstdint>
+#include <cuda.h>            // CUtensorMap (type only; no libcuda link)
+#include <cuda_runtime.h>
+
+namespace w25 {
+
+constexpr int R = 4;         // stencil radius, PAPER.md L411-414 (R = 4)
+
+// Stencil + PML constants, fp64-computed and rounded once to fp32 on the host
+// (R8).  Passed by value as a kernel parameter (constant bank).
+struct Coef {
+  float c0;                  // c_xyz
+  float cx[R], cy[R], cz[R]; // c_am, m = 1..4
+  float i2h[3];              // 1/(2 h_a)
+};
+
+// ---------------------------------------------------------------------------
+// Per-point arithmetic (SPEC.md L140-157 semantics; fp32 with FMA)
+// ---------------------------------------------------------------------------
+
+// Eq. 3: c_xyz u + sum_m c_am (u(+m) + u(-m)), pair sums
+// first (keeps mirror symmetry bitwise), axes x, y, z, m = 1..4.
+struct Nbr { float xm[R], xp[R], ym[R], yp[R], zm[R], zp[R]; };
+
+__device__ __forceinline__ float lap8(const Coef& k, float c, const Nbr& n) {
+  float L = __fmul_rn(k.c0, c);
+#pragma unroll
+  for (int m = 0; m < R; ++m) L = __fmaf_rn(k.cx[m], __fadd_rn(n.xp[m], n.xm[m]), L);
+#pragma unroll
+  for (int m = 0; m < R; ++m) L = __fmaf_rn(k.cy[m], __fadd_rn(n.yp[m], n.ym[m]), L);
+#pragma unroll
+  for (int m = 0; m < R; ++m) L = __fmaf_rn(k.cz[m], __fadd_rn(n.zp[m], n.zm[m]), L);
+  return L;
+}
+
+// inner update, Eq. 2 / SPEC.md L143: (2u - u_prev) + vdt2 L
+__device__ __forceinline__ float upd_inner(float L, float c, float up, float v) {
+  return __fmaf_rn(v, L, __fmaf_rn(2.0f, c, -up));
+}
+
+// one grad-eta . grad-u term: ((eta+ - eta-) / 2h) * ((u+ - u-) / 2h)
+__device__ __forceinline__ float gterm(float ep, float em, float u1p, float u1m, float i2h) {
+  return __fmul_rn(__fmul_rn(__fsub_rn(ep, em), i2h), __fmul_rn(__fsub_rn(u1p, u1m), i2h));
+}
+
+// PML update: ((2u - A u_prev) + vdt2 (L + g)) / B with a true
+// IEEE division (a reciprocal multiply drifts past the 1e-5 gate, R9)
+__device__ __forceinline__ float upd_pml(float L, float g, float c, float up, float v,
+                                         float A, float B) {
+  const float t = __fmaf_rn(-A, up, __fmul_rn(2.0f, c));
+  return __fdiv_rn(__fmaf_rn(v, __fadd_rn(L, g), t), B);
+}
+
+// Distance (cells) to the inner box along one axis, global coordinate i in
+// [-1, n]: 0 inside [w, n-w), 1..w in the PML, w+1 just outside (eta = 0).
+__device__ __forceinline__ int dist1(int i, int n, int w) {
+  return max(max(w - i, 0), i - (n - w - 1));
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers: shared-memory address, mbarrier, TMA (cp.async.bulk.tensor)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+               ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W25_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W25_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// 3-D tiled TMA load of one box into shared memory, completion signalled on
+// `bar` via complete_tx (bytes).  Out-of-bounds elements are zero-filled --
+// this supplies the x/y Dirichlet fringe for free.
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// Streaming 16-B store (evict-first: u_next is not re-read this step).
+__device__ __forceinline__ void st_cs_f4(float* p, float4 v) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w) : "memory");
+}
+
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+__device__ __forceinline__ float f4get(const float4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
+
+}  // namespace w25

@@ -1,0 +1,794 @@
+// wave.cu -- host side of the C ABI declared in include/wave.h.
+//
+// Owns: validation, fp64->fp32 constant tables, TMA descriptor encoding,
+// region/tile/chunk planning, launch of the streaming kernels (interior column
+// + x walls + y walls, forked on two streams and joined), the source kernel,
+// CUDA-graph capture of 2-step pairs, and the split-step calls used by the
+// z-slab multi-GPU driver.  No torch types cross this boundary.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cudaTypedefs.h>   // PFN_cuTensorMapEncodeTiled
+
+#include "../../include/wave.h"
+#include "aux_kernels.cuh"
+#include "stream.cuh"
+
+using namespace w25;
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static wave_status fail(wave_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(WAVE_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define CKST(expr)                          \
+  do {                                      \
+    wave_status s_ = (expr);                \
+    if (s_ != WAVE_OK) return s_;           \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// kernel configurations (tile shapes)
+// ---------------------------------------------------------------------------
+// interior column: 32x32 tiles, 2 rows per thread, 8-stage u ring, 4-stage p ring
+#define INNER_CFG 32, 32, 2, 8, 4
+// x walls (left/right, w wide in x): 16 x 32 tiles
+#define WALLX_CFG 16, 32, 2, 8, 4
+// y walls (front/back, w wide in y): 32 x 16 tiles
+#define WALLY_CFG 32, 16, 2, 8, 4
+
+enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_N = 3 };
+static const int KTX[KI_N] = {32, 16, 32};
+static const int KTY[KI_N] = {32, 32, 16};
+
+static constexpr double W8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0};
+static constexpr int MAX_W = 512;
+
+struct Maps {
+  CUtensorMap u[2];      // wavefield buffer b with halo box
+  CUtensorMap up[2];     // wavefield buffer b, tile box
+  CUtensorMap v;         // vdt2, tile box
+};
+
+struct Launch {          // one streaming-kernel launch
+  int ki = 0;
+  int nblk = 0;
+  StreamParams p{};
+};
+
+struct wave_plan {
+  wave_desc d{};
+  wave_layout_info L{};
+  int dev = 0, nsm = 148;
+  Coef coef{};
+  std::vector<float> tab_h;          // [3][w+2]
+  float* tab_d = nullptr;
+  float* buf[2] = {nullptr, nullptr};
+  float* vdt2 = nullptr;
+  bool bound = false, have_vel = false;
+  float dt = 0.f;
+  int cur = 0;                       // buf[cur] holds u^n
+  int64_t step = 0;
+  // source
+  bool src_set = false, src_local = false;
+  int64_t si = 0, sj = 0, sk = 0;
+  std::vector<float> wavelet;
+  float* inc_d = nullptr;
+  float* wl_d = nullptr;
+  int64_t ninc = 0;
+  unsigned long long* dstep = nullptr;
+  Stats* stats_d = nullptr;
+  // launch plans
+  Maps maps[KI_N];
+  int occ[KI_N] = {1, 1, 1};
+  std::vector<Launch> launches[3];   // [0] all planes, [1] edges, [2] interior
+  // streams / graphs
+  cudaStream_t side = nullptr, cap = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+};
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static wave_status get_encoder() {
+  if (g_encode) return WAVE_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess)
+    return fail(WAVE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return WAVE_OK;
+}
+
+static wave_status encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                            uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t b0, uint32_t b1) {
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(WAVE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return WAVE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// validation and constants
+// ---------------------------------------------------------------------------
+static double courant_number(const wave_desc& d, double vmax, double dt) {
+  // stability of leapfrog + Lap8: (V dt)^2 sum_a S/h_a^2 <= 4, S = max symbol
+  // of the 1-D operator = -(w0 + 2 sum_m w_m cos(m pi)) = 6.5016...
+  double S = -W8[0];
+  for (int m = 1; m <= 4; ++m) S -= 2.0 * W8[m] * ((m & 1) ? -1.0 : 1.0);
+  const double s = 1.0 / (d.hx * d.hx) + 1.0 / (d.hy * d.hy) + 1.0 / (d.hz * d.hz);
+  return vmax * dt * std::sqrt(S * s) / 2.0;   // must be <= 1
+}
+
+static wave_status validate(const wave_desc* d) {
+  if (!d) return fail(WAVE_ERR_CONFIG, "desc is NULL");
+  if (d->nx < 1 || d->ny < 1 || d->nz < 1) return fail(WAVE_ERR_CONFIG, "extents must be >= 1");
+  if (d->nx > (1 << 30) || d->ny > (1 << 30) || d->nz_global > (1 << 30))
+    return fail(WAVE_ERR_CONFIG, "extent too large");
+  if (d->nz_global < d->nz || d->z_offset < 0 || d->z_offset + d->nz > d->nz_global)
+    return fail(WAVE_ERR_CONFIG, "slab [z_offset, z_offset+nz) must lie in [0, nz_global)");
+  const int64_t w = d->pml_width;
+  const int64_t mn = std::min(d->nx, std::min(d->ny, d->nz_global));
+  if (w < 0 || 2 * w >= mn) return fail(WAVE_ERR_CONFIG, "need 0 <= 2w < min extent (w=%lld)", (long long)w);
+  if (w > MAX_W) return fail(WAVE_ERR_CONFIG, "pml_width > %d", MAX_W);
+  if (!(d->hx > 0 && d->hy > 0 && d->hz > 0) || !std::isfinite(d->hx) || !std::isfinite(d->hy) ||
+      !std::isfinite(d->hz))
+    return fail(WAVE_ERR_CONFIG, "spacing must be > 0");
+  if (!(d->dt >= 0.f) || !std::isfinite(d->dt)) return fail(WAVE_ERR_CONFIG, "dt must be >= 0 (0 = auto)");
+  if (!(d->eta_max >= 0) || !std::isfinite(d->eta_max)) return fail(WAVE_ERR_CONFIG, "eta_max must be >= 0");
+  if (d->kernel != WAVE_KERNEL_STREAM && d->kernel != WAVE_KERNEL_NAIVE)
+    return fail(WAVE_ERR_CONFIG, "unknown kernel %d", d->kernel);
+  if (d->dt == 0.f && (d->nz != d->nz_global)) return fail(WAVE_ERR_CONFIG, "auto dt needs a single-slab plan");
+  return WAVE_OK;
+}
+
+static void make_layout(const wave_desc& d, wave_layout_info* L) {
+  L->pitch_x = (d.nx + 3) / 4 * 4;
+  L->ghost_z = R;
+  L->planes = d.nz + 2 * R;
+  L->elems_u = L->planes * d.ny * L->pitch_x;
+  L->elems_vdt2 = d.nz * d.ny * L->pitch_x;
+  L->align_bytes = 128;
+}
+
+// fp64 -> fp32 once (R8)
+static void make_constants(const wave_desc& d, float dt, Coef* k, std::vector<float>* tab) {
+  const double ih2[3] = {1.0 / (d.hx * d.hx), 1.0 / (d.hy * d.hy), 1.0 / (d.hz * d.hz)};
+  k->c0 = (float)(W8[0] * (ih2[0] + ih2[1] + ih2[2]));
+  for (int m = 1; m <= 4; ++m) {
+    k->cx[m - 1] = (float)(W8[m] * ih2[0]);
+    k->cy[m - 1] = (float)(W8[m] * ih2[1]);
+    k->cz[m - 1] = (float)(W8[m] * ih2[2]);
+  }
+  k->i2h[0] = (float)(1.0 / (2.0 * d.hx));
+  k->i2h[1] = (float)(1.0 / (2.0 * d.hy));
+  k->i2h[2] = (float)(1.0 / (2.0 * d.hz));
+  const int w = d.pml_width, T = w + 2;
+  tab->assign(3 * T, 0.f);
+  for (int dd = 0; dd <= w; ++dd) {
+    const double r = w > 0 ? (double)dd / (double)w : 0.0;
+    const double eta = d.eta_max * r * r;                 // eta_max (d/w)^2, R2
+    (*tab)[dd] = (float)eta;
+    (*tab)[T + dd] = (float)(1.0 - eta * (double)dt);
+    (*tab)[2 * T + dd] = (float)(1.0 + eta * (double)dt);
+  }
+  (*tab)[w + 1] = 0.f;                                    // outside the domain (R4)
+  (*tab)[T + w + 1] = 1.f;
+  (*tab)[2 * T + w + 1] = 1.f;
+}
+
+// ---------------------------------------------------------------------------
+// launch planning
+// ---------------------------------------------------------------------------
+template <int TX, int TY, int TYT, int SU, int SP, int MODE>
+static void* kfn() { return (void*)k_stream<TX, TY, TYT, SU, SP, MODE>; }
+
+static void* kernel_ptr(int ki) {
+  switch (ki) {
+    case KI_INNER: return kfn<INNER_CFG, MODE_INNER>();
+    case KI_WALLX: return kfn<WALLX_CFG, MODE_WALL>();
+    default: return kfn<WALLY_CFG, MODE_WALL>();
+  }
+}
+static int kernel_threads(int ki) {
+  switch (ki) {
+    case KI_INNER: return StreamCfg<INNER_CFG>::NT;
+    case KI_WALLX: return StreamCfg<WALLX_CFG>::NT;
+    default: return StreamCfg<WALLY_CFG>::NT;
+  }
+}
+static size_t kernel_smem(int ki, int w) {
+  switch (ki) {
+    case KI_INNER: return StreamCfg<INNER_CFG>::smem_bytes(w);
+    case KI_WALLX: return StreamCfg<WALLX_CFG>::smem_bytes(w);
+    default: return StreamCfg<WALLY_CFG>::smem_bytes(w);
+  }
+}
+
+// z-chunk length minimising (waves x (chunk + warm-up)) for ncol columns over nz planes
+static int choose_cz(int64_t ncol, int nz, int resident) {
+  int best = nz;
+  double best_cost = 1e300;
+  for (int k = 1; k <= 256; ++k) {
+    const int cz = (nz + k - 1) / k;
+    if (cz < 8 && k > 1) break;
+    const int64_t nch = (nz + cz - 1) / cz;
+    const double waves = std::ceil((double)(ncol * nch) / std::max(1, resident));
+    const double cost = waves * (cz + 4.0);   // 8 warm-up planes ~ half a plane each
+    if (cost < best_cost * 0.999) { best_cost = cost; best = cz; }
+  }
+  return best;
+}
+
+struct ZRange { int z0, z1; };
+
+// Build the region list of one launch kind over a set of z ranges.
+static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 4>>& xy,
+                        const std::vector<ZRange>& zr, std::vector<Launch>* out);
+
+static wave_status build_launches(wave_plan* P) {
+  const int nx = (int)P->d.nx, ny = (int)P->d.ny, nz = (int)P->d.nz, w = P->d.pml_width;
+  std::vector<ZRange> all = {{0, nz}}, edges, inter;
+  if (nz <= 2 * R) {
+    edges = all;
+  } else {
+    edges = {{0, R}, {nz - R, nz}};
+    inter = {{R, nz - R}};
+  }
+  const std::vector<ZRange>* sets[3] = {&all, &edges, &inter};
+  for (int s = 0; s < 3; ++s) {
+    P->launches[s].clear();
+    if (sets[s]->empty()) continue;
+    add_regions(P, KI_INNER, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
+    if (w > 0) {
+      add_regions(P, KI_WALLX, {{0, w, w, ny - w}, {nx - w, nx, w, ny - w}}, *sets[s], &P->launches[s]);
+      add_regions(P, KI_WALLY, {{0, nx, 0, w}, {0, nx, ny - w, ny}}, *sets[s], &P->launches[s]);
+    }
+  }
+  return WAVE_OK;
+}
+
+static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 4>>& xy,
+                        const std::vector<ZRange>& zr, std::vector<Launch>* out) {
+  const int TX = KTX[ki], TY = KTY[ki];
+  // chunk length from the largest z range and the total column count
+  int64_t ncol = 0;
+  int nzmax = 0;
+  for (auto& b : xy) {
+    if (b[1] <= b[0] || b[3] <= b[2]) continue;
+    const int ax0 = b[0] & ~3;
+    ncol += (int64_t)((b[1] - ax0 + TX - 1) / TX) * ((b[3] - b[2] + TY - 1) / TY);
+  }
+  for (auto& z : zr) nzmax = std::max(nzmax, z.z1 - z.z0);
+  if (ncol == 0 || nzmax == 0) return;
+  const int resident = P->occ[ki] * P->nsm;
+  const int cz = choose_cz(ncol * (int64_t)zr.size(), nzmax, resident);
+
+  Launch Lc;
+  Lc.ki = ki;
+  StreamParams& p = Lc.p;
+  memset(&p, 0, sizeof p);
+  p.pitch = P->L.pitch_x;
+  p.plane = P->L.pitch_x * P->d.ny;
+  p.nx = (int)P->d.nx; p.ny = (int)P->d.ny; p.nzl = (int)P->d.nz;
+  p.nzg = (int)P->d.nz_global; p.zoff = (int)P->d.z_offset; p.w = P->d.pml_width;
+  p.k = P->coef;
+  p.tab = P->tab_d;
+  p.cz = cz;
+  int blk = 0;
+  auto flush = [&]() {
+    if (p.nreg == 0) return;
+    Lc.nblk = blk;
+    out->push_back(Lc);
+    p.nreg = 0;
+    blk = 0;
+  };
+  for (auto& z : zr) {
+    for (auto& b : xy) {
+      if (b[1] <= b[0] || b[3] <= b[2] || z.z1 <= z.z0) continue;
+      if (p.nreg == MAX_REGIONS) flush();
+      Region& g = p.reg[p.nreg++];
+      g.x0 = b[0]; g.x1 = b[1]; g.y0 = b[2]; g.y1 = b[3]; g.z0 = z.z0; g.z1 = z.z1;
+      g.ax0 = b[0] & ~3;
+      g.ntx = (b[1] - g.ax0 + TX - 1) / TX;
+      g.nty = (b[3] - b[2] + TY - 1) / TY;
+      g.nzc = (z.z1 - z.z0 + cz - 1) / cz;
+      g.blk0 = blk;
+      blk += g.ntx * g.nty * g.nzc;
+    }
+  }
+  flush();
+}
+
+// ---------------------------------------------------------------------------
+// step enqueue
+// ---------------------------------------------------------------------------
+static wave_status launch_stream(wave_plan* P, const Launch& Lc, int cur, cudaStream_t s) {
+  const Maps& M = P->maps[Lc.ki];
+  StreamParams p = Lc.p;
+  p.out = P->buf[1 - cur];
+  const dim3 grid(Lc.nblk), block(kernel_threads(Lc.ki));
+  const size_t smem = kernel_smem(Lc.ki, P->d.pml_width);
+  void* args[] = {(void*)&M.u[cur], (void*)&M.up[1 - cur], (void*)&M.v, (void*)&p};
+  CK(cudaLaunchKernel(kernel_ptr(Lc.ki), grid, block, args, smem, s));
+  return WAVE_OK;
+}
+
+static wave_status launch_naive(wave_plan* P, int cur, int z0, int z1, cudaStream_t s) {
+  if (z1 <= z0) return WAVE_OK;
+  NaiveParams np;
+  np.pitch = P->L.pitch_x;
+  np.plane = P->L.pitch_x * P->d.ny;
+  np.nx = (int)P->d.nx; np.ny = (int)P->d.ny; np.nzl = (int)P->d.nz;
+  np.nzg = (int)P->d.nz_global; np.zoff = (int)P->d.z_offset; np.w = P->d.pml_width;
+  np.z0 = z0;
+  np.k = P->coef;
+  np.tab = P->tab_d;
+  const dim3 grid((unsigned)((P->d.nx + 31) / 32), (unsigned)((P->d.ny + 3) / 4), (unsigned)(z1 - z0));
+  k_naive<<<grid, dim3(32, 4), 0, s>>>(P->buf[cur], P->buf[1 - cur], P->vdt2, np);
+  CK(cudaGetLastError());
+  return WAVE_OK;
+}
+
+static wave_status launch_source(wave_plan* P, int cur, cudaStream_t s) {
+  if (!P->src_set || !P->src_local || P->ninc == 0) return WAVE_OK;
+  const int64_t k = P->sk - P->d.z_offset;
+  const int64_t off = (k + R) * P->L.pitch_x * P->d.ny + P->sj * P->L.pitch_x + P->si;
+  k_source<<<1, 1, 0, s>>>(P->buf[1 - cur], off, P->inc_d, P->ninc, P->dstep);
+  CK(cudaGetLastError());
+  return WAVE_OK;
+}
+
+// which: 0 all planes, 1 edges, 2 interior
+static wave_status enqueue_compute(wave_plan* P, int which, int cur, cudaStream_t s) {
+  if (P->d.kernel == WAVE_KERNEL_NAIVE) {
+    const int nz = (int)P->d.nz;
+    if (which == 0 || (which == 1 && nz <= 2 * R)) return launch_naive(P, cur, 0, nz, s);
+    if (which == 1) {
+      CKST(launch_naive(P, cur, 0, R, s));
+      return launch_naive(P, cur, nz - R, nz, s);
+    }
+    return nz <= 2 * R ? WAVE_OK : launch_naive(P, cur, R, nz - R, s);
+  }
+  const std::vector<Launch>& Ls = P->launches[which];
+  if (Ls.empty()) return WAVE_OK;
+  // fork: the first launch (interior column) on s, the walls on the side stream
+  bool forked = false;
+  for (size_t i = 0; i < Ls.size(); ++i) {
+    if (Ls[i].ki == KI_INNER || Ls.size() == 1) {
+      CKST(launch_stream(P, Ls[i], cur, s));
+    } else {
+      if (!forked) {
+        CK(cudaEventRecord(P->ev_fork, s));
+        CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
+        forked = true;
+      }
+      CKST(launch_stream(P, Ls[i], cur, P->side));
+    }
+  }
+  if (forked) {
+    CK(cudaEventRecord(P->ev_join, P->side));
+    CK(cudaStreamWaitEvent(s, P->ev_join, 0));
+  }
+  return WAVE_OK;
+}
+
+static bool source_in(const wave_plan* P, int which) {
+  if (!P->src_set || !P->src_local) return false;
+  const int64_t k = P->sk - P->d.z_offset, nz = P->d.nz;
+  if (which == 0) return true;
+  const bool edge = nz <= 2 * R || k < R || k >= nz - R;
+  return which == 1 ? edge : !edge;
+}
+
+static wave_status enqueue_step(wave_plan* P, int cur, cudaStream_t s) {
+  CKST(enqueue_compute(P, 0, cur, s));
+  return launch_source(P, cur, s);
+}
+
+static wave_status ensure_graph(wave_plan* P, int parity) {
+  if (P->gexec[parity]) return WAVE_OK;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(P->cap, cudaStreamCaptureModeThreadLocal));
+  wave_status st = enqueue_step(P, parity, P->cap);
+  if (st == WAVE_OK) st = enqueue_step(P, 1 - parity, P->cap);
+  cudaError_t e = cudaStreamEndCapture(P->cap, &g);
+  if (st != WAVE_OK) { if (g) cudaGraphDestroy(g); return st; }
+  if (e != cudaSuccess) return fail(WAVE_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&P->gexec[parity], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(WAVE_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+  return WAVE_OK;
+}
+
+static void drop_graphs(wave_plan* P) {
+  for (int i = 0; i < 2; ++i)
+    if (P->gexec[i]) { cudaGraphExecDestroy(P->gexec[i]); P->gexec[i] = nullptr; }
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* wave_version(void) { return "wave25 0.1.0 sm_100a"; }
+
+const char* wave_last_error(void) { return g_err.c_str(); }
+
+wave_status wave_layout(const wave_desc* desc, wave_layout_info* out) {
+  CKST(validate(desc));
+  if (!out) return fail(WAVE_ERR_CONFIG, "out is NULL");
+  make_layout(*desc, out);
+  return WAVE_OK;
+}
+
+wave_status wave_decompose(const wave_desc* desc, wave_region* out) {
+  CKST(validate(desc));
+  if (!out) return fail(WAVE_ERR_CONFIG, "out is NULL");
+  const int64_t nx = desc->nx, ny = desc->ny, nz = desc->nz_global, w = desc->pml_width;
+  auto set = [&](int i, int kind, int64_t x, int64_t y, int64_t z, int64_t ex, int64_t ey, int64_t ez) {
+    out[i].kind = kind; out[i].reserved0 = 0;
+    out[i].lo[0] = x; out[i].lo[1] = y; out[i].lo[2] = z;
+    out[i].ext[0] = ex; out[i].ext[1] = ey; out[i].ext[2] = ez;
+  };
+  // Inner [w, n-w)^3; Top/Bottom full x,y, z-thickness w; Front/Back full
+  // x, y-thickness w, z in [w, nz-w); Left/Right x-thickness w, y in [w, ny-w), z in [w, nz-w)
+  set(0, WAVE_REGION_INNER, w, w, w, nx - 2 * w, ny - 2 * w, nz - 2 * w);
+  set(1, WAVE_REGION_TOP, 0, 0, 0, nx, ny, w);
+  set(2, WAVE_REGION_BOTTOM, 0, 0, nz - w, nx, ny, w);
+  set(3, WAVE_REGION_FRONT, 0, 0, w, nx, w, nz - 2 * w);
+  set(4, WAVE_REGION_BACK, 0, ny - w, w, nx, w, nz - 2 * w);
+  set(5, WAVE_REGION_LEFT, 0, w, w, w, ny - 2 * w, nz - 2 * w);
+  set(6, WAVE_REGION_RIGHT, nx - w, w, w, w, ny - 2 * w, nz - 2 * w);
+  return WAVE_OK;
+}
+
+wave_status wave_constants(const wave_desc* desc, float* c13, float* eta, float* A, float* B,
+                           float* inv2h) {
+  CKST(validate(desc));
+  if (!(desc->dt > 0.f)) return fail(WAVE_ERR_CONFIG, "wave_constants needs dt > 0");
+  Coef k;
+  std::vector<float> tab;
+  make_constants(*desc, desc->dt, &k, &tab);
+  const int w = desc->pml_width, T = w + 2;
+  if (c13) {
+    c13[0] = k.c0;
+    for (int m = 0; m < 4; ++m) { c13[1 + m] = k.cx[m]; c13[5 + m] = k.cy[m]; c13[9 + m] = k.cz[m]; }
+  }
+  for (int d = 0; d <= w; ++d) {
+    if (eta) eta[d] = tab[d];
+    if (A) A[d] = tab[T + d];
+    if (B) B[d] = tab[2 * T + d];
+  }
+  if (inv2h) for (int a = 0; a < 3; ++a) inv2h[a] = k.i2h[a];
+  return WAVE_OK;
+}
+
+wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
+  CKST(validate(desc));
+  if (!out) return fail(WAVE_ERR_CONFIG, "out is NULL");
+  *out = nullptr;
+  wave_plan* P = new (std::nothrow) wave_plan();
+  if (!P) return fail(WAVE_ERR_ALLOC, "host allocation failed");
+  P->d = *desc;
+  make_layout(P->d, &P->L);
+  P->dt = desc->dt;
+  auto bail = [&](wave_status st) { wave_plan_destroy(P); return st; };
+  cudaError_t e = cudaGetDevice(&P->dev);
+  if (e != cudaSuccess) return bail(fail(WAVE_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e)));
+  int major = 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, P->dev);
+  if (major != 10) return bail(fail(WAVE_ERR_CUDA, "this library is built for sm_100a (B200); device is sm_%d*", major));
+  cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, P->dev);
+  if (get_encoder() != WAVE_OK) return bail(WAVE_ERR_CUDA);
+  const int T = P->d.pml_width + 2;
+  if ((e = cudaMalloc(&P->tab_d, 3 * T * sizeof(float))) != cudaSuccess ||
+      (e = cudaMalloc(&P->dstep, sizeof(unsigned long long))) != cudaSuccess ||
+      (e = cudaMalloc(&P->stats_d, sizeof(Stats))) != cudaSuccess)
+    return bail(fail(WAVE_ERR_ALLOC, "cudaMalloc: %s", cudaGetErrorString(e)));
+  if ((e = cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&P->cap, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+    return bail(fail(WAVE_ERR_CUDA, "stream/event: %s", cudaGetErrorString(e)));
+  for (int ki = 0; ki < KI_N; ++ki) {
+    const size_t sm = kernel_smem(ki, P->d.pml_width);
+    if ((e = cudaFuncSetAttribute(kernel_ptr(ki), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
+      return bail(fail(WAVE_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr(ki), kernel_threads(ki), sm);
+    P->occ[ki] = std::max(1, occ);
+  }
+  *out = P;
+  return WAVE_OK;
+}
+
+void wave_plan_destroy(wave_plan* P) {
+  if (!P) return;
+  drop_graphs(P);
+  if (P->tab_d) cudaFree(P->tab_d);
+  if (P->dstep) cudaFree(P->dstep);
+  if (P->stats_d) cudaFree(P->stats_d);
+  if (P->inc_d) cudaFree(P->inc_d);
+  if (P->wl_d) cudaFree(P->wl_d);
+  if (P->side) cudaStreamDestroy(P->side);
+  if (P->cap) cudaStreamDestroy(P->cap);
+  if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+  if (P->ev_join) cudaEventDestroy(P->ev_join);
+  delete P;
+}
+
+static wave_status refresh_tables(wave_plan* P, cudaStream_t s) {
+  make_constants(P->d, P->dt, &P->coef, &P->tab_h);
+  CK(cudaMemcpyAsync(P->tab_d, P->tab_h.data(), P->tab_h.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));   // tab_h is pageable host memory
+  CKST(build_launches(P));
+  drop_graphs(P);
+  return WAVE_OK;
+}
+
+wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void* stream) {
+  if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
+  if (!u0 || !u1 || !vdt2 || u0 == u1) return fail(WAVE_ERR_CONFIG, "need two distinct wavefield buffers and vdt2");
+  for (const void* p : {(const void*)u0, (const void*)u1, (const void*)vdt2})
+    if (reinterpret_cast<uintptr_t>(p) % 128) return fail(WAVE_ERR_CONFIG, "buffers must be 128-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  P->buf[0] = u0; P->buf[1] = u1; P->vdt2 = vdt2;
+  CK(cudaMemsetAsync(u0, 0, P->L.elems_u * sizeof(float), s));
+  CK(cudaMemsetAsync(u1, 0, P->L.elems_u * sizeof(float), s));
+  CK(cudaMemsetAsync(vdt2, 0, P->L.elems_vdt2 * sizeof(float), s));
+  CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
+  const uint64_t pb = P->L.pitch_x * 4, plb = pb * P->d.ny;
+  for (int ki = 0; ki < KI_N; ++ki) {
+    const uint32_t TX = KTX[ki], TY = KTY[ki];
+    for (int b = 0; b < 2; ++b) {
+      CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
+      CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX, TY));
+    }
+    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, TX, TY));
+  }
+  P->cur = 0;
+  P->step = 0;
+  P->bound = true;
+  P->have_vel = false;
+  if (P->dt > 0.f) CKST(refresh_tables(P, s));
+  return WAVE_OK;
+}
+
+static wave_status rebuild_inc(wave_plan* P, cudaStream_t s) {
+  if (!P->src_set || !P->src_local || !P->have_vel) return WAVE_OK;
+  const int64_t k = P->sk - P->d.z_offset;
+  const float* vsrc = P->vdt2 + (k * P->d.ny + P->sj) * P->L.pitch_x + P->si;
+  const int64_t ns = (int64_t)P->wavelet.size();
+  P->ninc = ns;
+  if (ns == 0) return WAVE_OK;
+  CK(cudaMemcpyAsync(P->wl_d, P->wavelet.data(), ns * sizeof(float), cudaMemcpyHostToDevice, s));
+  k_inc<<<(unsigned)std::min<int64_t>((ns + 255) / 256, 1024), 256, 0, s>>>(P->inc_d, P->wl_d, ns, vsrc);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return WAVE_OK;
+}
+
+static wave_status field_stats(wave_plan* P, const float* base, int64_t rows, int positive, Stats* h,
+                               cudaStream_t s) {
+  Stats init{0u, 0x7f7fffffu, 0u, 0u};
+  CK(cudaMemcpyAsync(P->stats_d, &init, sizeof init, cudaMemcpyHostToDevice, s));
+  const int64_t n = rows * P->d.nx;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4 * 148 * 8));
+  k_stats<<<blocks, 256, 0, s>>>(base, P->L.pitch_x, (int)P->d.nx, rows, positive, P->stats_d);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h, P->stats_d, sizeof(Stats), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return WAVE_OK;
+}
+
+wave_status wave_set_velocity(wave_plan* P, const float* vel, int32_t where, void* stream) {
+  if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
+  if (!P->bound) return fail(WAVE_ERR_STATE, "bind buffers before wave_set_velocity");
+  if (!vel) return fail(WAVE_ERR_CONFIG, "vel is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t rows = P->d.ny * P->d.nz;
+  CK(cudaMemcpy2DAsync(P->vdt2, P->L.pitch_x * 4, vel, P->d.nx * 4, P->d.nx * 4, rows,
+                       where == WAVE_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  Stats st;
+  CKST(field_stats(P, P->vdt2, rows, 1, &st, s));
+  P->have_vel = false;
+  if (st.bad) return fail(WAVE_ERR_CONFIG, "velocity must be finite and > 0 (%u bad values)", st.bad);
+  float vmax;
+  memcpy(&vmax, &st.max_bits, 4);
+  float dt = P->d.dt;
+  if (dt == 0.f) dt = (float)(0.4 * std::min(P->d.hx, std::min(P->d.hy, P->d.hz)) / (double)vmax);
+  const double cn = courant_number(P->d, vmax, dt);
+  if (cn > 1.0) return fail(WAVE_ERR_CONFIG, "dt = %g violates the Courant limit (ratio %.4f > 1)", dt, cn);
+  P->dt = dt;
+  k_vdt2<<<4 * 148, 256, 0, s>>>(P->vdt2, P->L.pitch_x, (int)P->d.nx, rows, (double)dt);
+  CK(cudaGetLastError());
+  CKST(refresh_tables(P, s));
+  P->have_vel = true;
+  CKST(rebuild_inc(P, s));
+  return WAVE_OK;
+}
+
+wave_status wave_set_source(wave_plan* P, int64_t i, int64_t j, int64_t k, const float* wl, int64_t ns,
+                            void* stream) {
+  if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
+  if (!P->have_vel) return fail(WAVE_ERR_STATE, "set the velocity before the source");
+  const int64_t w = P->d.pml_width;
+  if (i < w || i >= P->d.nx - w || j < w || j >= P->d.ny - w || k < w || k >= P->d.nz_global - w)
+    return fail(WAVE_ERR_CONFIG, "source (%lld,%lld,%lld) must lie inside the inner region", (long long)i,
+                (long long)j, (long long)k);
+  if (ns < 0 || (ns > 0 && !wl)) return fail(WAVE_ERR_CONFIG, "bad wavelet");
+  cudaStream_t s = (cudaStream_t)stream;
+  P->wavelet.assign(wl, wl + ns);
+  if (P->inc_d) { cudaFree(P->inc_d); P->inc_d = nullptr; }
+  if (P->wl_d) { cudaFree(P->wl_d); P->wl_d = nullptr; }
+  if (ns > 0) {
+    CK(cudaMalloc(&P->inc_d, ns * sizeof(float)));
+    CK(cudaMalloc(&P->wl_d, ns * sizeof(float)));
+  }
+  P->si = i; P->sj = j; P->sk = k;
+  P->src_set = true;
+  P->src_local = k >= P->d.z_offset && k < P->d.z_offset + P->d.nz;
+  P->ninc = 0;
+  drop_graphs(P);
+  return rebuild_inc(P, s);
+}
+
+wave_status wave_set_state(wave_plan* P, const float* uprev, const float* ucur, int32_t where, void* stream) {
+  if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
+  if (!P->bound) return fail(WAVE_ERR_STATE, "bind buffers first");
+  cudaStream_t s = (cudaStream_t)stream;
+  const cudaMemcpyKind kind = where == WAVE_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const float* src[2] = {ucur, uprev};
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaMemsetAsync(P->buf[b], 0, P->L.elems_u * sizeof(float), s));
+    if (src[b])
+      CK(cudaMemcpy2DAsync(P->buf[b] + R * P->L.pitch_x * P->d.ny, P->L.pitch_x * 4, src[b], P->d.nx * 4,
+                           P->d.nx * 4, P->d.ny * P->d.nz, kind, s));
+  }
+  CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
+  P->cur = 0;
+  P->step = 0;
+  return WAVE_OK;
+}
+
+static wave_status ready(const wave_plan* P) {
+  if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
+  if (!P->bound) return fail(WAVE_ERR_STATE, "bind buffers first");
+  if (!P->have_vel) return fail(WAVE_ERR_STATE, "set the velocity first");
+  return WAVE_OK;
+}
+
+wave_status wave_step(wave_plan* P, int64_t nsteps, void* stream) {
+  CKST(ready(P));
+  if (nsteps < 0) return fail(WAVE_ERR_CONFIG, "nsteps < 0");
+  if (P->d.nz != P->d.nz_global) return fail(WAVE_ERR_STATE, "multi-slab plan: use the split-step calls");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t left = nsteps;
+  if (left >= 2) {
+    CKST(ensure_graph(P, P->cur));     // a 2-step graph returns to the same parity
+    while (left >= 2) {
+      CK(cudaGraphLaunch(P->gexec[P->cur], s));
+      left -= 2;
+      P->step += 2;
+    }
+  }
+  if (left == 1) {
+    CKST(enqueue_step(P, P->cur, s));
+    P->cur = 1 - P->cur;
+    P->step += 1;
+  }
+  return WAVE_OK;
+}
+
+wave_status wave_step_edges(wave_plan* P, void* stream) {
+  CKST(ready(P));
+  cudaStream_t s = (cudaStream_t)stream;
+  CKST(enqueue_compute(P, 1, P->cur, s));
+  if (source_in(P, 1)) CKST(launch_source(P, P->cur, s));
+  return WAVE_OK;
+}
+
+wave_status wave_step_interior(wave_plan* P, void* stream) {
+  CKST(ready(P));
+  cudaStream_t s = (cudaStream_t)stream;
+  CKST(enqueue_compute(P, 2, P->cur, s));
+  if (source_in(P, 2)) CKST(launch_source(P, P->cur, s));
+  return WAVE_OK;
+}
+
+wave_status wave_step_finish(wave_plan* P) {
+  CKST(ready(P));
+  P->cur = 1 - P->cur;
+  P->step += 1;
+  return WAVE_OK;
+}
+
+wave_status wave_halo_views(const wave_plan* P, float** send_lo, float** send_hi, float** recv_lo,
+                            float** recv_hi, int64_t* count) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
+  const int64_t plane = P->L.pitch_x * P->d.ny, nz = P->d.nz;
+  float* b = P->buf[1 - P->cur];      // the buffer wave_step_edges writes
+  if (send_lo) *send_lo = b + R * plane;
+  if (send_hi) *send_hi = b + nz * plane;
+  if (recv_lo) *recv_lo = b;
+  if (recv_hi) *recv_hi = b + (nz + R) * plane;
+  if (count) *count = R * plane;
+  return WAVE_OK;
+}
+
+wave_status wave_read(const wave_plan* P, int32_t which, float* dst, int32_t where, void* stream) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
+  if (!dst || (which != 0 && which != 1)) return fail(WAVE_ERR_CONFIG, "bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  const float* b = P->buf[which == 0 ? P->cur : 1 - P->cur] + R * P->L.pitch_x * P->d.ny;
+  CK(cudaMemcpy2DAsync(dst, P->d.nx * 4, b, P->L.pitch_x * 4, P->d.nx * 4, P->d.ny * P->d.nz,
+                       where == WAVE_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  if (where == WAVE_MEM_HOST) CK(cudaStreamSynchronize(s));
+  return WAVE_OK;
+}
+
+wave_status wave_field_ptr(const wave_plan* P, int32_t which, float** out) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
+  if (!out || (which != 0 && which != 1)) return fail(WAVE_ERR_CONFIG, "bad arguments");
+  *out = P->buf[which == 0 ? P->cur : 1 - P->cur] + R * P->L.pitch_x * P->d.ny;
+  return WAVE_OK;
+}
+
+wave_status wave_check_finite(wave_plan* P, float* h_maxabs, void* stream) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
+  Stats st;
+  CKST(field_stats(P, P->buf[P->cur] + R * P->L.pitch_x * P->d.ny, P->d.ny * P->d.nz, 0, &st,
+                   (cudaStream_t)stream));
+  float mx;
+  memcpy(&mx, &st.max_bits, 4);
+  if (h_maxabs) *h_maxabs = st.bad ? NAN : mx;
+  if (st.bad)
+    return fail(WAVE_ERR_UNSTABLE, "non-finite wavefield at step %lld (%u values)", (long long)P->step, st.bad);
+  return WAVE_OK;
+}
+
+int64_t wave_step_index(const wave_plan* P) { return P ? P->step : -1; }
+
+float wave_get_dt(const wave_plan* P) { return P ? P->dt : 0.f; }
+
+int32_t wave_launches_per_step(const wave_plan* P) {
+  if (!P) return -1;
+  int n = 0;
+  if (P->d.kernel == WAVE_KERNEL_NAIVE) n = 1;
+  else n = (int)P->launches[0].size();
+  if (P->src_set && P->src_local && P->ninc > 0) n += 1;
+  return n;
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+"""z-slab domain decomposition across GPUs (not in the paper,
+which is single-GPU).
+
+The extended domain is cut into contiguous z-slabs, one per rank (z is the
+outermost axis, so a slab face is one contiguous block of 4 planes).  Per time
+step only u^n's 4 boundary planes cross ranks: u^{n-1} and vdt2 are read at
+the centre only and eta is computed in-register.  The exchange is a pairwise
+send/recv with no reduction:
+
+    edges kernel (planes [0,4) and [nz-4,nz))  -> stream E
+    send those planes to the neighbours' ghost planes, receive theirs
+                                                  (NCCL over NVLink, after E)
+    interior kernel (planes [4, nz-4))          -> stream I (overlaps the exchange)
+    join, role swap
+
+`slab_bounds` and `halo_exchange` are backend-agnostic (NCCL with CUDA
+tensors, gloo with CPU tensors) so the decomposition logic is tested on CPU
+with world_size 2 (tests/test_dist_cpu.py).
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+GHOST = 4   # stencil radius R = 4
+
+
+def slab_bounds(nz_global: int, rank: int, world: int) -> tuple[int, int]:
+    """(z_offset, nz_local) of `rank`: near-equal contiguous slabs, the first
+    nz_global % world ranks one plane thicker.  Every slab needs >= 4 planes so
+    that its ghost planes come from one neighbour."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(nz_global, world)
+    if base < GHOST:
+        raise ValueError(f"nz_global={nz_global} too small for {world} slabs (need >= {GHOST} planes each)")
+    nz = base + (1 if rank < extra else 0)
+    off = rank * base + min(rank, extra)
+    return off, nz
+
+
+def halo_exchange(send_lo: Optional[torch.Tensor], send_hi: Optional[torch.Tensor],
+                  recv_lo: Optional[torch.Tensor], recv_hi: Optional[torch.Tensor],
+                  rank: int, world: int, group=None, stage_on_host: bool = False):
+    """Send my lowest/highest 4 planes to rank-1 / rank+1 and receive theirs
+    into my lower/upper ghost planes.  Returns the list of work handles
+    (call .wait() on each).  With stage_on_host, CUDA blocks go through host
+    copies (for gloo, which has no CUDA P2P)."""
+    ops = []
+    staged = []
+    def _s(t):
+        if stage_on_host and t.is_cuda:
+            h = t.detach().cpu()
+            return h
+        return t
+    def _r(t):
+        if stage_on_host and t.is_cuda:
+            h = torch.empty(t.shape, dtype=t.dtype)
+            staged.append((h, t))
+            return h
+        return t
+    if rank > 0:
+        ops.append(dist.P2POp(dist.isend, _s(send_lo), rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, _r(recv_lo), rank - 1, group))
+    if rank < world - 1:
+        ops.append(dist.P2POp(dist.isend, _s(send_hi), rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, _r(recv_hi), rank + 1, group))
+    if not ops:
+        return []
+    works = dist.batch_isend_irecv(ops)
+    if staged:
+        for wk in works:
+            wk.wait()
+        for h, t in staged:
+            t.copy_(h)
+        return []
+    return works
+
+
+class SlabRunner:
+    """One rank's slab of a distributed run (NCCL, one process per GPU).
+
+    The step is split so the halo exchange of the 4 edge planes overlaps the
+    interior kernel: edges on `s_edge` -> NCCL send/recv (ordered after the
+    edges by running under `s_edge`) while the interior runs on the current
+    stream; both are joined before the role swap.
+    """
+
+    def __init__(self, plan, rank: int, world: int, group=None, stage_on_host: bool = False):
+        self.plan = plan
+        self.rank, self.world, self.group = rank, world, group
+        self.stage_on_host = stage_on_host
+        self.s_edge = torch.cuda.Stream(device=plan.device)
+
+    def step(self, n: int = 1) -> None:
+        main = torch.cuda.current_stream(self.plan.device)
+        for _ in range(n):
+            self.s_edge.wait_stream(main)
+            self.plan.step_edges(stream=self.s_edge)
+            if self.world > 1:
+                send_lo, send_hi, recv_lo, recv_hi = self.plan.halo_views()
+                with torch.cuda.stream(self.s_edge):
+                    works = halo_exchange(send_lo, send_hi, recv_lo, recv_hi, self.rank, self.world,
+                                          self.group, self.stage_on_host)
+                    for wk in works:
+                        wk.wait()      # makes s_edge wait for the NCCL kernels
+            self.plan.step_interior(stream=main)
+            main.wait_stream(self.s_edge)
+            self.plan.step_finish()

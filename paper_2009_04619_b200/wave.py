@@ -1,0 +1,171 @@
+"""WavePlan: torch-owned device buffers + the C ABI (marshalling only).
+
+PyTorch provides device memory and streams; every step of the method runs in
+libwave25.so's CUDA kernels (include/wave.h).  Arrays passed in are copied to
+the device by the library (host pointers) or read in place (device tensors).
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _abi
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+def _as_input(a, shape, device):
+    """Return (pointer, where, keepalive) for a dense fp32 array of `shape`."""
+    if isinstance(a, torch.Tensor):
+        t = a.detach()
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"shape {tuple(t.shape)} != {tuple(shape)}")
+        t = t.to(dtype=torch.float32).contiguous()
+        if t.is_cuda:
+            if t.device != device:
+                t = t.to(device)
+            return t.data_ptr(), _abi.WAVE_MEM_DEVICE, t
+        return t.data_ptr(), _abi.WAVE_MEM_HOST, t
+    arr = np.ascontiguousarray(a, dtype=np.float32)
+    if arr.shape != tuple(shape):
+        raise ValueError(f"shape {arr.shape} != {tuple(shape)}")
+    return arr.ctypes.data, _abi.WAVE_MEM_HOST, arr
+
+
+class WavePlan:
+    """One grid (or one z-slab of a grid) on one GPU.
+
+    nx, ny, nz   extended extents of this plan (nz = slab planes)
+    w            PML width;  h spacing (scalar or (hx, hy, hz));  dt (0 = auto)
+    eta_max      PML damping maximum (1/s);  kernel "stream" | "naive"
+    nz_global, z_offset   slab position (defaults: single slab)
+    """
+
+    def __init__(self, nx, ny, nz, w, h, dt, eta_max=4.0, kernel="stream",
+                 nz_global=None, z_offset=0, device=None, stream=None):
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        kern = {"stream": _abi.WAVE_KERNEL_STREAM, "naive": _abi.WAVE_KERNEL_NAIVE}[kernel]
+        self.desc = _abi.make_desc(nx, ny, nz, w, h, float(np.float32(dt)), eta_max, kern,
+                                   nz_global, z_offset)
+        self.layout = _abi.wave_layout(self.desc)
+        self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        self.shape = (self.nz, self.ny, self.nx)
+        self._plan = None
+        with torch.cuda.device(self.device):
+            L = self.layout
+            self.bufs = [torch.empty(L.elems_u, dtype=torch.float32, device=self.device) for _ in range(2)]
+            self.vdt2 = torch.empty(L.elems_vdt2, dtype=torch.float32, device=self.device)
+            self._plan = _abi.wave_plan_create(self.desc)
+            _abi.wave_plan_bind(self._plan, self.bufs[0].data_ptr(), self.bufs[1].data_ptr(),
+                                self.vdt2.data_ptr(), _stream_handle(stream))
+        self._keep = []
+
+    # ---- inputs ---------------------------------------------------------
+    def set_velocity(self, vel, stream=None) -> None:
+        ptr, where, keep = _as_input(vel, self.shape, self.device)
+        with torch.cuda.device(self.device):
+            _abi.wave_set_velocity(self._plan, ptr, where, _stream_handle(stream))
+        del keep
+
+    def set_source(self, i, j, k, wavelet, stream=None) -> None:
+        wl = np.ascontiguousarray(np.asarray(wavelet, dtype=np.float32).ravel())
+        with torch.cuda.device(self.device):
+            _abi.wave_set_source(self._plan, i, j, k, wl.ctypes.data, wl.size, _stream_handle(stream))
+
+    def set_state(self, uprev=None, ucur=None, stream=None) -> None:
+        """Initial u^{-1} / u^0 (None = zero); both host or both device arrays."""
+        given = [a for a in (uprev, ucur) if a is not None]
+        conv = [_as_input(a, self.shape, self.device) for a in given]
+        if len({c[1] for c in conv}) > 1:
+            raise ValueError("uprev and ucur must both be host or both device arrays")
+        where = conv[0][1] if conv else _abi.WAVE_MEM_HOST
+        it = iter(conv)
+        ptrs = [None if a is None else next(it)[0] for a in (uprev, ucur)]
+        with torch.cuda.device(self.device):
+            _abi.wave_set_state(self._plan, ptrs[0], ptrs[1], where, _stream_handle(stream))
+        del conv
+
+    # ---- stepping -------------------------------------------------------
+    def step(self, n: int = 1, stream=None) -> None:
+        with torch.cuda.device(self.device):
+            _abi.wave_step(self._plan, n, _stream_handle(stream))
+
+    def step_edges(self, stream=None) -> None:
+        _abi.wave_step_edges(self._plan, _stream_handle(stream))
+
+    def step_interior(self, stream=None) -> None:
+        _abi.wave_step_interior(self._plan, _stream_handle(stream))
+
+    def step_finish(self) -> None:
+        _abi.wave_step_finish(self._plan)
+
+    # ---- outputs --------------------------------------------------------
+    def _buffer_view(self, ptr: int) -> torch.Tensor:
+        L = self.layout
+        for b in self.bufs:
+            off = ptr - b.data_ptr()
+            if 0 <= off < b.numel() * 4:
+                start = off // 4
+                v = b[start:start + self.nz * self.ny * L.pitch_x]
+                return v.view(self.nz, self.ny, L.pitch_x)[:, :, :self.nx]
+        raise RuntimeError("field pointer outside the plan's buffers")
+
+    def field(self, which: int = 0) -> torch.Tensor:
+        """Zero-copy [nz, ny, nx] view of u^n (which=0) or u^{n-1} (which=1)."""
+        return self._buffer_view(_abi.wave_field_ptr(self._plan, which))
+
+    def read(self, which: int = 0, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Dense copy of u^n / u^{n-1}; `out` may be a CUDA or (pinned) CPU tensor."""
+        if out is None:
+            out = torch.empty(self.shape, dtype=torch.float32, device=self.device)
+        where = _abi.WAVE_MEM_DEVICE if out.is_cuda else _abi.WAVE_MEM_HOST
+        with torch.cuda.device(self.device):
+            _abi.wave_read(self._plan, which, out.data_ptr(), where, _stream_handle(stream))
+        return out
+
+    def halo_views(self):
+        """(send_lo, send_hi, recv_lo, recv_hi) torch views of 4-plane blocks."""
+        a, b, c, d, n = _abi.wave_halo_views(self._plan)
+        out = []
+        for p in (a, b, c, d):
+            for buf in self.bufs:
+                off = p - buf.data_ptr()
+                if 0 <= off < buf.numel() * 4:
+                    out.append(buf[off // 4: off // 4 + n])
+                    break
+        return tuple(out)
+
+    def check_finite(self, stream=None) -> float:
+        with torch.cuda.device(self.device):
+            return _abi.wave_check_finite(self._plan, _stream_handle(stream))
+
+    @property
+    def step_index(self) -> int:
+        return _abi.wave_step_index(self._plan)
+
+    @property
+    def dt(self) -> float:
+        return _abi.wave_get_dt(self._plan)
+
+    @property
+    def launches_per_step(self) -> int:
+        return _abi.wave_launches_per_step(self._plan)
+
+    def close(self) -> None:
+        if self._plan is not None:
+            torch.cuda.synchronize(self.device)
+            _abi.wave_plan_destroy(self._plan)
+            self._plan = None
+
+    def __del__(self):
+        try:
+            if self._plan is not None:
+                _abi.wave_plan_destroy(self._plan)
+                self._plan = None
+        except Exception:
+            pass

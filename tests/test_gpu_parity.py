@@ -1,0 +1,296 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by
+element on identical seeded inputs.  Gate (BASELINE.json north_star): fp32,
+max |u_gpu - u_oracle| / max |u_oracle| <= 1e-5 after the configured steps.
+Stream and naive kernels must agree bitwise; z-slab plans must agree bitwise
+with the single-slab plan."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def WavePlan(*a, **k):
+    from paper_2009_04619_b200.wave import WavePlan as WP
+    return WP(*a, **k)
+
+
+def rel_linf(got, ref):
+    m = float(np.abs(ref).max())
+    return float(np.abs(got.astype(np.float64) - ref).max()) / (m if m > 0 else 1.0)
+
+
+def run_gpu(s, steps, u0=None, um1=None, kernel="stream", V=None, wl=None):
+    V = synth.velocity(s) if V is None else V
+    wl = synth.wavelet_for(s, max(steps, 1)) if wl is None else wl
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel)
+    p.set_velocity(V)
+    p.set_source(*s.source, wl)
+    if u0 is not None or um1 is not None:
+        p.set_state(um1, u0)
+    p.step(steps)
+    out = (p.read(0).cpu().numpy(), p.read(1).cpu().numpy())
+    p.close()
+    return out
+
+
+def run_oracle(s, steps, u0=None, um1=None, V=None, wl=None):
+    V = synth.velocity(s) if V is None else V
+    wl = synth.wavelet_for(s, max(steps, 1)) if wl is None else wl
+    g = oracle.make_geom(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    u, up, st, _ = oracle.propagate(g, V, wl, steps, s.source, u0=u0, uprev0=um1)
+    assert st == 0
+    return u, up
+
+
+@pytest.mark.parametrize("kernel", ["stream", "naive"])
+def test_c1_point_source(kernel):
+    # BASELINE.json configs[0]: 64^3, const V, Ricker, 10 steps
+    s = synth.scenario("C1")
+    g, gp = run_gpu(s, s.steps, kernel=kernel)
+    r, rp = run_oracle(s, s.steps)
+    assert rel_linf(g, r) <= TOL and rel_linf(gp, rp) <= TOL
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("steps", [1, 10, 100])
+def test_c1_random_state(seed, steps):
+    # O(1) amplitude everywhere, incl. the PML (SURVEY.md §8(d) C1 extras)
+    s = synth.scenario("C1")
+    sh = (s.nz, s.ny, s.nx)
+    u0, um1 = synth.random_state(sh, 2 * seed), synth.random_state(sh, 2 * seed + 1)
+    g, _ = run_gpu(s, steps, u0, um1)
+    r, _ = run_oracle(s, steps, u0, um1)
+    assert rel_linf(g, r) <= TOL, rel_linf(g, r)
+
+
+@pytest.mark.parametrize("name,steps", [("RAGGED", 40), ("SPEC48", 50)])
+def test_ragged_and_spec_scenarios(name, steps):
+    s = synth.scenario(name)
+    sh = (s.nz, s.ny, s.nx)
+    u0 = synth.random_state(sh, 3)
+    g, gp = run_gpu(s, steps, u0)
+    r, rp = run_oracle(s, steps, u0)
+    assert rel_linf(g, r) <= TOL and rel_linf(gp, rp) <= TOL
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("RAGGED", dict(w=0)),                               # no PML at all
+    ("RAGGED", dict(nx=9, ny=11, nz=10, w=2, src=(4, 5, 5))),   # smaller than one tile
+    ("RAGGED", dict(nx=37, ny=70, nz=12, w=3, src=(18, 35, 6))),  # nz < 2*9, thin slab
+    ("RAGGED", dict(w=20, nx=70, ny=45, nz=53, src=(35, 22, 26))),  # w wider than a wall tile
+    ("C1", dict(h=(10.0, 7.5, 12.5), eta_max=30.0)),      # anisotropic spacing, strong PML
+])
+def test_edge_geometries(name, kw):
+    s = synth.scenario(name, **kw)
+    sh = (s.nz, s.ny, s.nx)
+    u0, um1 = synth.random_state(sh, 11), synth.random_state(sh, 12)
+    g, _ = run_gpu(s, 7, u0, um1)
+    r, _ = run_oracle(s, 7, u0, um1)
+    assert rel_linf(g, r) <= TOL
+
+
+@pytest.mark.parametrize("name", ["C1", "RAGGED"])
+def test_stream_equals_naive_bitwise(name):
+    s = synth.scenario(name)
+    sh = (s.nz, s.ny, s.nx)
+    u0, um1 = synth.random_state(sh, 21), synth.random_state(sh, 22)
+    a, ap = run_gpu(s, 20, u0, um1, kernel="stream")
+    b, bp = run_gpu(s, 20, u0, um1, kernel="naive")
+    assert np.array_equal(a, b) and np.array_equal(ap, bp)
+
+
+def test_mirror_symmetry_bitwise():
+    n = 33
+    s = synth.scenario("C1", nx=n, ny=n, nz=n, w=8, steps=60)
+    g, _ = run_gpu(s, s.steps)
+    assert np.abs(g).max() > 0
+    for ax in range(3):
+        assert np.array_equal(g, np.flip(g, axis=ax)), ax
+
+
+def test_zero_and_one_step():
+    s = synth.scenario("RAGGED")
+    sh = (s.nz, s.ny, s.nx)
+    u0, um1 = synth.random_state(sh, 1), synth.random_state(sh, 2)
+    g0, gp0 = run_gpu(s, 0, u0, um1)
+    assert np.array_equal(g0, u0) and np.array_equal(gp0, um1)
+    g1, gp1 = run_gpu(s, 1, u0, um1)
+    r1, _ = run_oracle(s, 1, u0, um1)
+    assert rel_linf(g1, r1) <= TOL and np.array_equal(gp1, u0)
+
+
+def test_source_only_first_step_exact():
+    # from the zero state one step leaves exactly fp32(vdt2[src] w[0]) at the source
+    s = synth.scenario("RAGGED")
+    wl = np.array([0.75], np.float32)
+    g, _ = run_gpu(s, 1, wl=wl)
+    r, _ = run_oracle(s, 1, wl=wl)
+    assert np.array_equal(g, r)
+    assert np.count_nonzero(g) == 1
+
+
+def test_graph_replay_matches_stepwise():
+    s = synth.scenario("C1")
+    sh = (s.nz, s.ny, s.nx)
+    u0 = synth.random_state(sh, 4)
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    p.set_velocity(synth.velocity(s))
+    p.set_source(*s.source, synth.wavelet_for(s, 30))
+    p.set_state(None, u0)
+    p.step(13)                       # 6 graph pairs + 1
+    a = p.read(0).cpu().numpy()
+    p.set_state(None, u0)
+    for _ in range(13):
+        p.step(1)
+    b = p.read(0).cpu().numpy()
+    assert p.step_index == 13
+    p.close()
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("nslab", [2, 3])
+def test_slabs_on_one_gpu_bitwise(nslab):
+    # z-slab plans + edges/interior split + device-to-device halo exchange == single plan
+    from paper_2009_04619_b200.dist import slab_bounds
+    s = synth.scenario("RAGGED")
+    sh = (s.nz, s.ny, s.nx)
+    u0, um1 = synth.random_state(sh, 7), synth.random_state(sh, 8)
+    V = synth.velocity(s)
+    wl = synth.wavelet_for(s, 25)
+    plans = []
+    for r in range(nslab):
+        off, nzl = slab_bounds(s.nz, r, nslab)
+        p = WavePlan(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
+        p.set_velocity(V[off:off + nzl])
+        p.set_source(*s.source, wl)
+        p.set_state(um1[off:off + nzl], u0[off:off + nzl])
+        plans.append((p, off, nzl))
+    # initial halos: ghosts of u^0 come from the neighbours' edge planes
+    for r, (p, off, nzl) in enumerate(plans):
+        cur = p.field(0)
+        full = torch.from_numpy(u0).cuda()
+        buf = [b for b in p.bufs if b.data_ptr() <= cur.data_ptr() < b.data_ptr() + 4 * b.numel()][0]
+        plane = s.ny * p.layout.pitch_x
+        v = buf.view(-1, s.ny, p.layout.pitch_x)
+        if r > 0:
+            v[0:4, :, :s.nx] = full[off - 4:off]
+        if r < nslab - 1:
+            v[nzl + 4:nzl + 8, :, :s.nx] = full[off + nzl:off + nzl + 4]
+    for n in range(25):
+        for p, _, _ in plans:
+            p.step_edges()
+        for r, (p, off, nzl) in enumerate(plans):
+            send_lo, send_hi, recv_lo, recv_hi = p.halo_views()
+            if r > 0:
+                plans[r - 1][0].halo_views()[3].copy_(send_lo)
+            if r < nslab - 1:
+                plans[r + 1][0].halo_views()[2].copy_(send_hi)
+        for p, _, _ in plans:
+            p.step_interior()
+            p.step_finish()
+    got = np.concatenate([p.read(0).cpu().numpy() for p, _, _ in plans], axis=0)
+    ref, _ = run_gpu(s, 25, u0, um1, wl=wl)
+    for p, _, _ in plans:
+        p.close()
+    assert np.array_equal(got, ref)
+
+
+def test_unstable_eta_max_detected():
+    from paper_2009_04619_b200 import WaveError
+    from paper_2009_04619_b200._abi import WAVE_ERR_UNSTABLE
+    s = synth.scenario("C1", nx=24, ny=24, nz=24, w=6, eta_max=100.0, src=(12, 12, 12))
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    p.set_velocity(synth.velocity(s))
+    p.set_state(None, synth.random_state((24, 24, 24), 3))
+    p.step(400)
+    with pytest.raises(WaveError) as e:
+        p.check_finite()
+    assert e.value.status == WAVE_ERR_UNSTABLE
+    p.close()
+
+
+def test_courant_rejected():
+    from paper_2009_04619_b200 import WaveError
+    s = synth.scenario("C1", dt=5e-3)           # dt V / h = 1.0 > 0.4529
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    with pytest.raises(WaveError):
+        p.set_velocity(synth.velocity(s))
+    p.close()
+
+
+def test_auto_dt_matches_oracle_rule():
+    s = synth.scenario("SPEC48")
+    V = synth.velocity(s)
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, 0.0, s.eta_max)
+    p.set_velocity(V)
+    assert np.float32(p.dt) == oracle.dt_auto(s.h, V)
+    p.close()
+
+
+def _full_size_slab_check(sname, steps, zt_list, seed=0):
+    """Full-size GPU run; oracle recomputes sampled z-slabs.  The oracle slab
+    is the target planes plus 4*steps planes of margin on each side, whose
+    ghost planes hold the initial state: after `steps` steps the target planes
+    are exact (the contamination from stale ghosts moves 4 planes per step)."""
+    s = synth.scenario(sname)
+    sh = (s.nz, s.ny, s.nx)
+    u0 = synth.random_state(sh, seed)
+    um1 = synth.random_state(sh, seed + 1)
+    V = synth.velocity(s)
+    wl = synth.wavelet_for(s, steps)
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    p.set_velocity(V)
+    p.set_source(*s.source, wl)
+    p.set_state(um1, u0)
+    p.step(steps)
+    gpu = p.field(0)
+    R = 4
+    M = R * steps
+    worst = 0.0
+    for zt0, zt1 in zt_list:
+        a, b = max(zt0 - M, 0), min(zt1 + M, s.nz)
+        nzl = b - a
+        g = oracle.make_geom(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=a)
+
+        def padded(full):
+            q = np.zeros((nzl + 8, s.ny + 8, s.nx + 8), np.float32)
+            lo, hi = max(a - R, 0), min(b + R, s.nz)
+            q[lo - (a - R):hi - (a - R), R:-R, R:-R] = full[lo:hi]
+            return q
+        uu, upp = padded(u0), padded(um1)
+        vd = oracle.vdt2(V[a:b], s.dt)
+        for n in range(steps):
+            assert oracle.step_padded(g, uu, upp, vd, s.source, wl[n]) == 0
+            uu, upp = upp, uu
+        ref = uu[R + zt0 - a:R + zt1 - a, R:-R, R:-R]
+        got = gpu[zt0:zt1].cpu().numpy()
+        worst = max(worst, rel_linf(got, ref))
+    p.close()
+    return worst
+
+
+@pytest.mark.parametrize("sname", ["C2", "C3"])
+def test_full_size_sampled_slabs(sname):
+    # BASELINE.json configs[1] / configs[2] at full size, the bench's launch
+    # configuration (stream kernels, CUDA graphs); sampled z ranges cover the
+    # top cap, the middle (source plane) and the bottom cap.
+    s = synth.scenario(sname)
+    n = s.nz
+    zt = [(0, 6), (n // 2 - 3, n // 2 + 3), (n - 6, n)]
+    err = _full_size_slab_check(sname, 5, zt)
+    assert err <= TOL, err
