@@ -61,10 +61,11 @@ __device__ __forceinline__ float upd_pml(float L, float g, float c, float up, fl
   return __fdiv_rn(__fmaf_rn(v, __fadd_rn(L, g), t), B);
 }
 
-// Distance (cells) to the inner box along one axis, global coordinate i in
-// [-1, n]: 0 inside [w, n-w), 1..w in the PML, w+1 just outside (eta = 0).
+// Distance (cells) to the inner box along one axis: 0 inside [w, n-w), 1..w
+// in the PML, w+1 outside the domain (eta = 0; clamped so that points of a
+// ragged tile beyond the grid index the (w+2)-entry tables safely).
 __device__ __forceinline__ int dist1(int i, int n, int w) {
-  return max(max(w - i, 0), i - (n - w - 1));
+  return min(max(max(w - i, 0), i - (n - w - 1)), w + 1);
 }
 
 // ---------------------------------------------------------------------------
