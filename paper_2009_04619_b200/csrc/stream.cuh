@@ -6,24 +6,24 @@
 //    so co-resident CTAs are xy-neighbours at similar z and the 4-cell halo
 //    rows they re-read come from L2, not HBM.
 //  * u planes (tile + 4-cell halo, (TX+8) x (TY+8) floats) arrive by TMA
-//    (cp.async.bulk.tensor.3d) into an SU-stage shared-memory ring, one
-//    mbarrier per stage.  Out-of-bounds x/y cells are zero-filled by TMA, so
-//    the Dirichlet fringe costs nothing.  u_prev and vdt2 planes (tile only)
-//    arrive the same way into an SP-stage ring.  Thread 0 refills the stage
-//    freed by the plane just finished after one __syncthreads per plane.
+//    (cp.async.bulk.tensor.3d) into a 9-stage shared-memory ring, one mbarrier
+//    per stage; out-of-bounds x/y cells are zero-filled by TMA, so the
+//    Dirichlet fringe costs nothing.  u_prev and vdt2 planes (tile only)
+//    arrive the same way into a 3-stage ring.  9 = the z-window 2R+1, so with
+//    the plane loop unrolled 9x every stage index, register-queue slot and
+//    mbarrier parity is a compile-time constant (no address arithmetic).
 //  * Each thread owns 4 consecutive x points (one float4) x TYT rows and keeps
-//    the 9 z-planes u(z-4..z+4) of its points in a register queue with fixed
-//    slots (slot = plane mod 9, loop unrolled 9x so every slot index is a
-//    compile-time constant) -- the paper's st_reg_fixed idea (PAPER.md
-//    L735-775).  x neighbours come from 2 LDS.128 per row (left/right float4),
-//    y neighbours from 8 LDS.128 per thread-row group, z neighbours from
-//    registers.
-//  * MODE_INNER: region = inner xy footprint; planes inside the inner z range
-//    take the inner update (no per-point branches); the z-PML caps (global
-//    planes k < w or k >= nz-w) take the PML update with plane-uniform eta
-//    (one warp-uniform branch per plane).  MODE_WALL: x/y PML walls, every
-//    point takes the PML update with eta on the 7-point star evaluated from
-//    integer distances (no stored eta array, 0 HBM bytes).
+//    u(z-4..z+4) of its points in a 9-slot register queue with fixed slots --
+//    the paper's st_reg_fixed idea.  x neighbours: 2
+//    LDS.128 per row; y neighbours: 8 LDS.128 per thread; z: registers.
+//  * All 4*TYT points of a plane are evaluated as interleaved independent
+//    FMA chains; the PML-vs-inner choice is one uniform branch per plane.
+//  * MODE_INNER: region = inner xy footprint over all z; planes in the inner z
+//    range take the inner update; the z-PML caps (global k < w, k >= nz-w)
+//    take the PML update with plane-uniform eta through a non-inlined
+//    function (keeps the hot loop's code small).  MODE_WALL: x/y PML walls,
+//    every point takes the PML update with eta on the 7-point star evaluated
+//    from integer distances (no stored eta array, 0 extra HBM bytes).
 #pragma once
 #include "common.cuh"
 
@@ -39,19 +39,22 @@ struct Region {
 };
 
 constexpr int MAX_REGIONS = 4;
+constexpr int SU = 9;           // u ring stages  (= 2R+1)
+constexpr int SP = 3;           // u_prev/vdt2 ring stages (divides 9)
 
 struct StreamParams {
   float* out;                   // u_next buffer (= u_prev buffer), padded layout base
   int64_t pitch, plane;         // row / plane pitch in floats
   int nx, ny, nzl, nzg, zoff, w;
   int cz;                       // z-chunk length
+  int pf;                       // L2 prefetch distance (planes beyond the TMA rings; 0 = off)
   int nreg;
   Region reg[MAX_REGIONS];
   Coef k;
   const float* tab;             // [3][w+2]: eta_d, A_d, B_d (d = 0..w), eta_{w+1} = 0
 };
 
-template <int TX, int TY, int TYT, int SU, int SP>
+template <int TX, int TY, int TYT>
 struct StreamCfg {
   static constexpr int LX = TX / 4;               // float4 lanes across x
   static constexpr int LY = TY / TYT;             // thread rows
@@ -65,17 +68,35 @@ struct StreamCfg {
   static size_t smem_bytes(int w) { return TAB_OFF + 3 * (w + 2) * 4; }
   static_assert(TX % 4 == 0 && TY % TYT == 0, "tile shape");
   static_assert((U_STAGE * 4) % 128 == 0 && (P_STAGE * 4) % 128 == 0, "TMA smem alignment");
-  static_assert(SU >= 8, "u ring must hold the 8 warm-up planes");
   static_assert(NT % 32 == 0, "whole warps");
 };
 
-template <int TX, int TY, int TYT, int SU, int SP, int MODE>
-__global__ void __launch_bounds__(StreamCfg<TX, TY, TYT, SU, SP>::NT)
+// Plane-uniform constants of a z-PML cap plane seen from the inner xy footprint.
+struct CapC { float ex, ezp, ezm, A, B; };
+
+// PML update of one float4 row inside a z cap (inner x,y => eta(x+-1) =
+// eta(y+-1) = eta_dz); same arithmetic as the naive kernel's PML branch.
+__device__ __noinline__ float4 cap_update(float4 L, float4 C, float4 up, float4 v, float4 xp, float4 xm,
+                                          float4 yp, float4 ym, float4 zp, float4 zm, CapC cc,
+                                          float i2hx, float i2hy, float i2hz) {
+  float res[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float g = __fadd_rn(__fadd_rn(gterm(cc.ex, cc.ex, f4get(xp, c), f4get(xm, c), i2hx),
+                                        gterm(cc.ex, cc.ex, f4get(yp, c), f4get(ym, c), i2hy)),
+                              gterm(cc.ezp, cc.ezm, f4get(zp, c), f4get(zm, c), i2hz));
+    res[c] = upd_pml(f4get(L, c), g, f4get(C, c), f4get(up, c), f4get(v, c), cc.A, cc.B);
+  }
+  return make_float4(res[0], res[1], res[2], res[3]);
+}
+
+template <int TX, int TY, int TYT, int MODE>
+__global__ void __launch_bounds__(StreamCfg<TX, TY, TYT>::NT)
 k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1)
          const __grid_constant__ CUtensorMap tm_up,   // u^{n-1}, box (TX, TY, 1)
          const __grid_constant__ CUtensorMap tm_v,    // vdt2, box (TX, TY, 1)
-         const StreamParams P) {
-  using C = StreamCfg<TX, TY, TYT, SU, SP>;
+         const __grid_constant__ StreamParams P) {
+  using C = StreamCfg<TX, TY, TYT>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* su = reinterpret_cast<float*>(smem_raw);
   float* sup = su + SU * C::U_STAGE;
@@ -89,7 +110,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
   int b = blockIdx.x, ri = 0;
 #pragma unroll 1
   while (ri + 1 < P.nreg && b >= P.reg[ri + 1].blk0) ++ri;
-  const Region G = P.reg[ri];
+  const Region& G = P.reg[ri];
   b -= G.blk0;
   const int ncol = G.ntx * G.nty;
   const int zc = b / ncol;
@@ -106,15 +127,18 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
   const int ly = tid / C::LX;
   const int gx = tx0 + 4 * lx;              // first x of my float4
   const int gy = ty0 + ly * TYT;            // first y of my rows
-  const int scol = 4 * lx + R;              // smem column of my float4
-  const int srow0 = ly * TYT + R;           // smem row of my first row
+  // smem offsets (floats) of my float4 in row 0 of the tile, u stage / p stage
+  const int uo = (ly * TYT + R) * C::SW + 4 * lx + R;
+  const int po = (ly * TYT) * TX + 4 * lx;
 
   // ---- setup: barriers, PML tables, prologue TMA ------------------------
   if (tid == 0) {
     prefetch_tmap(&tm_u);
     prefetch_tmap(&tm_up);
     prefetch_tmap(&tm_v);
+#pragma unroll
     for (int s = 0; s < SU; ++s) mbar_init(&bar_u[s], 1);
+#pragma unroll
     for (int s = 0; s < SP; ++s) mbar_init(&bar_p[s], 1);
     fence_mbar_init();
   }
@@ -123,20 +147,22 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
 
   const uint64_t pol_u = policy_evict_last();    // u^n: re-read (halo) by neighbours
   const uint64_t pol_s = policy_evict_first();   // u^{n-1}, vdt2: streamed once
-  auto issue_u = [&](int p) {                     // plane p (local z), p >= zs-4
-    const int s = (p - zs + R) % SU;
+  // plane p (local z, p >= zs-4) lives in u stage (p - zs + 4) % 9
+  auto issue_u = [&](int p, int s) {
     mbar_arrive_expect_tx(&bar_u[s], C::U_STAGE * 4);
     tma_load_3d(su + s * C::U_STAGE, &tm_u, &bar_u[s], tx0 - R, ty0 - R, p + R, pol_u);
   };
-  auto issue_p = [&](int p) {
-    const int s = (p - zs) % SP;
+  // plane p (p >= zs) lives in p stage (p - zs) % 3
+  auto issue_p = [&](int p, int s) {
     mbar_arrive_expect_tx(&bar_p[s], 2 * C::P_STAGE * 4);
     tma_load_3d(sup + s * C::P_STAGE, &tm_up, &bar_p[s], tx0, ty0, p + R, pol_s);
     tma_load_3d(sv + s * C::P_STAGE, &tm_v, &bar_p[s], tx0, ty0, p, pol_s);
   };
   if (tid == 0) {
-    for (int p = zs - R; p < zs - R + SU && p <= ze + R - 1; ++p) issue_u(p);
-    for (int p = zs; p < zs + SP && p < ze; ++p) issue_p(p);
+    for (int s = 0; s < SU; ++s)
+      if (zs - R + s <= ze + R - 1) issue_u(zs - R + s, s);      // planes zs-4 .. zs+4
+    for (int s = 0; s < SP; ++s)
+      if (zs + s < ze) issue_p(zs + s, s);                       // planes zs .. zs+2
   }
 
   // ---- per-thread geometry: store mask, PML distances --------------------
@@ -149,154 +175,195 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
       if (x >= G.x0 && x < G.x1 && y >= G.y0 && y < G.y1) mask |= 1u << (r * 4 + c);
     }
   const bool full = mask == (TYT * 4 == 32 ? 0xffffffffu : ((1u << (TYT * 4)) - 1u));
-  int dxs[6], dys[TYT + 2];                  // distances at x = gx-1..gx+4, y = gy-1..gy+TYT
+  // wall mode: z-independent parts of the 7-point eta star per point
+  int dxy[TYT][4], ixp[TYT][4], ixm[TYT][4], iyp[TYT][4], iym[TYT][4];
   if (MODE == MODE_WALL) {
 #pragma unroll
-    for (int c = 0; c < 6; ++c) dxs[c] = dist1(gx - 1 + c, P.nx, P.w);
+    for (int r = 0; r < TYT; ++r) {
+      const int dy = dist1(gy + r, P.ny, P.w);
+      const int dyp = dist1(gy + r + 1, P.ny, P.w), dym = dist1(gy + r - 1, P.ny, P.w);
 #pragma unroll
-    for (int r = 0; r < TYT + 2; ++r) dys[r] = dist1(gy - 1 + r, P.ny, P.w);
+      for (int c = 0; c < 4; ++c) {
+        const int dx = dist1(gx + c, P.nx, P.w);
+        dxy[r][c] = max(dx, dy);
+        ixp[r][c] = max(dist1(gx + c + 1, P.nx, P.w), dy);
+        ixm[r][c] = max(dist1(gx + c - 1, P.nx, P.w), dy);
+        iyp[r][c] = max(dx, dyp);
+        iym[r][c] = max(dx, dym);
+      }
+    }
   }
-  float* outp = P.out + (int64_t)gy * P.pitch + gx;
+  float* optr = P.out + (int64_t)(zs + R) * P.plane + (int64_t)gy * P.pitch + gx;
 
-  // ---- warm-up: planes zs-4 .. zs+3 into queue slots 0..7 ----------------
+  // ---- warm-up: planes zs-4 .. zs+3 (stages 0..7, first use) -> queue ----
   float4 q[9][TYT];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    const int p = zs - R + s;
-    const int st = (p - zs + R) % SU;
-    mbar_wait(&bar_u[st], ((p - zs + R) / SU) & 1);
+    mbar_wait(&bar_u[s], 0);
 #pragma unroll
-    for (int r = 0; r < TYT; ++r)
-      q[s][r] = lds4(su + st * C::U_STAGE + (srow0 + r) * C::SW + scol);
+    for (int r = 0; r < TYT; ++r) q[s][r] = lds4(su + s * C::U_STAGE + uo + r * C::SW);
   }
   __syncthreads();                           // stages of planes zs-4..zs-1 are free
   if (tid == 0) {
     fence_proxy_async_smem();
-    for (int p = zs - R + SU; p < zs + SU; ++p)
-      if (p <= ze + R - 1) issue_u(p);
+#pragma unroll
+    for (int s = 0; s < R; ++s)
+      if (zs + 5 + s <= ze + R - 1) issue_u(zs + 5 + s, s);      // planes zs+5 .. zs+8
   }
 
   const Coef& K = P.k;
-  // ---- main loop over planes, unrolled 9x (fixed register slots) ---------
+  // ---- main loop over planes, unrolled 9x (fixed slots / stages) ---------
 #pragma unroll 1
-  for (int z0 = zs; z0 < ze; z0 += 9) {
+  for (int z0 = zs, j = 0; z0 < ze; z0 += 9, ++j) {
 #pragma unroll
     for (int s = 0; s < 9; ++s) {
       const int z = z0 + s;
       if (z >= ze) break;
-      // slot of plane z+o is (s + 4 + o) mod 9 (compile-time)
+      const int sl = (s + 8) % 9;            // slot/stage of the leading plane z+4
+      const int sc = (s + 4) % 9;            // slot/stage of plane z
       // 1. leading plane z+4 -> queue
-      {
-        const int p = z + R;
-        const int st = (p - zs + R) % SU;
-        mbar_wait(&bar_u[st], ((p - zs + R) / SU) & 1);
+      mbar_wait(&bar_u[sl], (j + (s >= 1 ? 1 : 0)) & 1);
 #pragma unroll
-        for (int r = 0; r < TYT; ++r)
-          q[(s + 8) % 9][r] = lds4(su + st * C::U_STAGE + (srow0 + r) * C::SW + scol);
-      }
-      // 2. u^{n-1} and vdt2 of plane z
-      float4 upv[TYT], vv[TYT];
-      {
-        const int st = (z - zs) % SP;
-        mbar_wait(&bar_p[st], ((z - zs) / SP) & 1);
+      for (int r = 0; r < TYT; ++r) q[sl][r] = lds4(su + sl * C::U_STAGE + uo + r * C::SW);
+
+      // 2. Laplacian of all 4*TYT points (interleaved chains)
+      const float* S = su + sc * C::U_STAGE + uo;
+      float4 Y[TYT + 2 * R];                 // rows -4 .. TYT+3 at my float4
 #pragma unroll
-        for (int r = 0; r < TYT; ++r) {
-          upv[r] = lds4(sup + st * C::P_STAGE + (ly * TYT + r) * TX + 4 * lx);
-          vv[r] = lds4(sv + st * C::P_STAGE + (ly * TYT + r) * TX + 4 * lx);
-        }
+      for (int jj = 0; jj < TYT + 2 * R; ++jj) {
+        if (jj >= R && jj < R + TYT) Y[jj] = q[sc][jj - R];
+        else Y[jj] = lds4(S + (jj - R) * C::SW);
       }
-      // 3. compute plane z from the u stage of plane z
-      const float* S = su + ((z - zs + R) % SU) * C::U_STAGE;
-      float4 Y[TYT + 2 * R];                 // rows gy-4 .. gy+TYT+3 at my float4
-#pragma unroll
-      for (int j = 0; j < TYT + 2 * R; ++j) {
-        if (j >= R && j < R + TYT) Y[j] = q[(s + 4) % 9][j - R];
-        else Y[j] = lds4(S + (srow0 - R + j) * C::SW + scol);
-      }
-      const int kg = z + P.zoff;
-      bool pml_plane = false;
-      float A_c = 1.f, B_c = 1.f, ez_p = 0.f, ez_m = 0.f, ex_c = 0.f;
-      int dzk = 0, dzp = 0, dzm = 0;
-      if (MODE == MODE_INNER) {
-        pml_plane = (kg < P.w) || (kg >= P.nzg - P.w);
-        if (pml_plane) {
-          dzk = dist1(kg, P.nzg, P.w);
-          A_c = stab[TABN + dzk];
-          B_c = stab[2 * TABN + dzk];
-          ex_c = stab[dzk];
-          ez_p = stab[dist1(kg + 1, P.nzg, P.w)];
-          ez_m = stab[dist1(kg - 1, P.nzg, P.w)];
-        }
-      } else {
-        dzk = dist1(kg, P.nzg, P.w);
-        dzp = dist1(kg + 1, P.nzg, P.w);
-        dzm = dist1(kg - 1, P.nzg, P.w);
-      }
+      float4 Lf[TYT], Rf[TYT];
 #pragma unroll
       for (int r = 0; r < TYT; ++r) {
-        const float* Srow = S + (srow0 + r) * C::SW + scol;
-        const float4 Lf = lds4(Srow - 4);
-        const float4 Ce = Y[R + r];
-        const float4 Rf = lds4(Srow + 4);
-        const float X[12] = {Lf.x, Lf.y, Lf.z, Lf.w, Ce.x, Ce.y, Ce.z, Ce.w, Rf.x, Rf.y, Rf.z, Rf.w};
-        float res[4];
+        Lf[r] = lds4(S + r * C::SW - 4);
+        Rf[r] = lds4(S + r * C::SW + 4);
+      }
+      float L[TYT][4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          Nbr n;
+      for (int r = 0; r < TYT; ++r)
 #pragma unroll
-          for (int m = 1; m <= R; ++m) {
-            n.xm[m - 1] = X[4 + c - m];
-            n.xp[m - 1] = X[4 + c + m];
-            n.ym[m - 1] = f4get(Y[R + r - m], c);
-            n.yp[m - 1] = f4get(Y[R + r + m], c);
-            n.zm[m - 1] = f4get(q[(s + 4 - m + 9) % 9][r], c);
-            n.zp[m - 1] = f4get(q[(s + 4 + m) % 9][r], c);
-          }
-          const float uc = X[4 + c];
-          const float L = lap8(K, uc, n);
-          const float upc = f4get(upv[r], c), vc = f4get(vv[r], c);
-          if (MODE == MODE_INNER) {
-            if (!pml_plane) {
-              res[c] = upd_inner(L, uc, upc, vc);
-            } else {
-              // inner xy footprint inside a z cap: eta(x +- 1) = eta(y +- 1) = eta_dz
-              const float g = __fadd_rn(__fadd_rn(gterm(ex_c, ex_c, n.xp[0], n.xm[0], K.i2h[0]),
-                                                  gterm(ex_c, ex_c, n.yp[0], n.ym[0], K.i2h[1])),
-                                        gterm(ez_p, ez_m, n.zp[0], n.zm[0], K.i2h[2]));
-              res[c] = upd_pml(L, g, uc, upc, vc, A_c, B_c);
-            }
-          } else {
-            const int dxc = dxs[c + 1], dyc = dys[r + 1];
-            const int dxy = max(dxc, dyc);
-            const int d = max(dxy, dzk);
-            const float exp_ = stab[max(max(dxs[c + 2], dyc), dzk)];
-            const float exm = stab[max(max(dxs[c], dyc), dzk)];
-            const float eyp = stab[max(max(dxc, dys[r + 2]), dzk)];
-            const float eym = stab[max(max(dxc, dys[r]), dzk)];
-            const float ezp = stab[max(dxy, dzp)];
-            const float ezm = stab[max(dxy, dzm)];
-            const float g = __fadd_rn(__fadd_rn(gterm(exp_, exm, n.xp[0], n.xm[0], K.i2h[0]),
-                                                gterm(eyp, eym, n.yp[0], n.ym[0], K.i2h[1])),
-                                      gterm(ezp, ezm, n.zp[0], n.zm[0], K.i2h[2]));
-            res[c] = upd_pml(L, g, uc, upc, vc, stab[TABN + d], stab[2 * TABN + d]);
-          }
-        }
-        // 4. store u_next (streaming; masked on ragged tiles)
-        float* o = outp + (int64_t)(z + R) * P.plane + (int64_t)r * P.pitch;
-        if (full) {
-          st_cs_f4(o, make_float4(res[0], res[1], res[2], res[3]));
-        } else {
+        for (int c = 0; c < 4; ++c) L[r][c] = __fmul_rn(K.c0, f4get(Y[R + r], c));
+#pragma unroll
+      for (int m = 1; m <= R; ++m)
+#pragma unroll
+        for (int r = 0; r < TYT; ++r) {
+          const float X[12] = {Lf[r].x, Lf[r].y, Lf[r].z, Lf[r].w, Y[R + r].x, Y[R + r].y,
+                               Y[R + r].z, Y[R + r].w, Rf[r].x, Rf[r].y, Rf[r].z, Rf[r].w};
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (mask & (1u << (r * 4 + c))) o[c] = res[c];
+            L[r][c] = __fmaf_rn(K.cx[m - 1], __fadd_rn(X[4 + c + m], X[4 + c - m]), L[r][c]);
+        }
+#pragma unroll
+      for (int m = 1; m <= R; ++m)
+#pragma unroll
+        for (int r = 0; r < TYT; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            L[r][c] = __fmaf_rn(K.cy[m - 1], __fadd_rn(f4get(Y[R + r + m], c), f4get(Y[R + r - m], c)), L[r][c]);
+#pragma unroll
+      for (int m = 1; m <= R; ++m)
+#pragma unroll
+        for (int r = 0; r < TYT; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            L[r][c] = __fmaf_rn(K.cz[m - 1],
+                                __fadd_rn(f4get(q[(s + 4 + m) % 9][r], c), f4get(q[(s + 4 - m + 9) % 9][r], c)),
+                                L[r][c]);
+
+      // 3. u^{n-1}, vdt2 of plane z
+      const int sp = s % 3;
+      mbar_wait(&bar_p[sp], (j + s / 3) & 1);
+      float4 upv[TYT], vv[TYT];
+#pragma unroll
+      for (int r = 0; r < TYT; ++r) {
+        upv[r] = lds4(sup + sp * C::P_STAGE + po + r * TX);
+        vv[r] = lds4(sv + sp * C::P_STAGE + po + r * TX);
+      }
+
+      // 4. update (one uniform branch per plane) and store
+      const int kg = z + P.zoff;
+      float4 res[TYT];
+      if (MODE == MODE_INNER) {
+        if (kg >= P.w && kg < P.nzg - P.w) {
+#pragma unroll
+          for (int r = 0; r < TYT; ++r) {
+            const float4 Cu = Y[R + r];
+            res[r] = make_float4(upd_inner(L[r][0], Cu.x, upv[r].x, vv[r].x),
+                                 upd_inner(L[r][1], Cu.y, upv[r].y, vv[r].y),
+                                 upd_inner(L[r][2], Cu.z, upv[r].z, vv[r].z),
+                                 upd_inner(L[r][3], Cu.w, upv[r].w, vv[r].w));
+          }
+        } else {
+          const int dz = dist1(kg, P.nzg, P.w);
+          CapC cc;
+          cc.ex = stab[dz];
+          cc.ezp = stab[dist1(kg + 1, P.nzg, P.w)];
+          cc.ezm = stab[dist1(kg - 1, P.nzg, P.w)];
+          cc.A = stab[TABN + dz];
+          cc.B = stab[2 * TABN + dz];
+#pragma unroll
+          for (int r = 0; r < TYT; ++r) {
+            const float4 Cu = Y[R + r];
+            const float4 xp = make_float4(Cu.y, Cu.z, Cu.w, Rf[r].x);
+            const float4 xm = make_float4(Lf[r].w, Cu.x, Cu.y, Cu.z);
+            res[r] = cap_update(make_float4(L[r][0], L[r][1], L[r][2], L[r][3]), Cu, upv[r], vv[r], xp, xm,
+                                Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], cc,
+                                K.i2h[0], K.i2h[1], K.i2h[2]);
+          }
+        }
+      } else {
+        const int dzk = dist1(kg, P.nzg, P.w);
+        const int dzp = dist1(kg + 1, P.nzg, P.w), dzm = dist1(kg - 1, P.nzg, P.w);
+#pragma unroll
+        for (int r = 0; r < TYT; ++r) {
+          const float4 Cu = Y[R + r];
+          const float X[12] = {Lf[r].x, Lf[r].y, Lf[r].z, Lf[r].w, Cu.x, Cu.y,
+                               Cu.z, Cu.w, Rf[r].x, Rf[r].y, Rf[r].z, Rf[r].w};
+          float o[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int d = max(dxy[r][c], dzk);
+            const float exp_ = stab[max(ixp[r][c], dzk)], exm = stab[max(ixm[r][c], dzk)];
+            const float eyp = stab[max(iyp[r][c], dzk)], eym = stab[max(iym[r][c], dzk)];
+            const float ezp = stab[max(dxy[r][c], dzp)], ezm = stab[max(dxy[r][c], dzm)];
+            const float g = __fadd_rn(
+                __fadd_rn(gterm(exp_, exm, X[5 + c], X[3 + c], K.i2h[0]),
+                          gterm(eyp, eym, f4get(Y[R + r + 1], c), f4get(Y[R + r - 1], c), K.i2h[1])),
+                gterm(ezp, ezm, f4get(q[(s + 5) % 9][r], c), f4get(q[(s + 3) % 9][r], c), K.i2h[2]));
+            o[c] = upd_pml(L[r][c], g, X[4 + c], f4get(upv[r], c), f4get(vv[r], c), stab[TABN + d],
+                           stab[2 * TABN + d]);
+          }
+          res[r] = make_float4(o[0], o[1], o[2], o[3]);
         }
       }
+      if (full) {
+#pragma unroll
+        for (int r = 0; r < TYT; ++r) st_cs_f4(optr + r * P.pitch, res[r]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < TYT; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (mask & (1u << (r * 4 + c))) optr[r * P.pitch + c] = f4get(res[r], c);
+      }
+      optr += P.plane;
+
       // 5. release the stages of plane z, refill them
       __syncthreads();
       if (tid == 0) {
         fence_proxy_async_smem();
-        if (z + SU <= ze + R - 1) issue_u(z + SU);
-        if (z + SP < ze) issue_p(z + SP);
+        if (z + SU <= ze + R - 1) issue_u(z + SU, sc);
+        if (z + SP < ze) issue_p(z + SP, sp);
+        if (P.pf > 0) {
+          const int pu = z + SU + P.pf, pp = z + SP + P.pf;
+          if (pu <= ze + R - 1) tma_prefetch_3d(&tm_u, tx0 - R, ty0 - R, pu + R);
+          if (pp < ze) {
+            tma_prefetch_3d(&tm_up, tx0, ty0, pp + R);
+            tma_prefetch_3d(&tm_v, tx0, ty0, pp);
+          }
+        }
       }
     }
   }

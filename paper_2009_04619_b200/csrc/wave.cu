@@ -54,16 +54,60 @@ static wave_status fail(wave_status st, const char* fmt, ...) {
 // ---------------------------------------------------------------------------
 // kernel configurations (tile shapes)
 // ---------------------------------------------------------------------------
-// interior column: 32x32 tiles, 2 rows per thread, 8-stage u ring, 4-stage p ring
-#define INNER_CFG 32, 32, 2, 8, 4
-// x walls (left/right, w wide in x): 16 x 32 tiles
-#define WALLX_CFG 16, 32, 2, 8, 4
-// y walls (front/back, w wide in y): 32 x 16 tiles
-#define WALLY_CFG 32, 16, 2, 8, 4
+struct KInfo {
+  void* fn;
+  int tx, ty, nt;
+  size_t (*smem)(int w);
+  const char* name;
+};
+
+template <int TX, int TY, int TYT, int MODE>
+static KInfo kinfo(const char* name) {
+  return KInfo{(void*)k_stream<TX, TY, TYT, MODE>, TX, TY, StreamCfg<TX, TY, TYT>::NT,
+               &StreamCfg<TX, TY, TYT>::smem_bytes, name};
+}
+
+// interior-column variants (WAVE25_INNER_TILE selects one; default first)
+static const KInfo* inner_variants(int* n) {
+  static const KInfo v[] = {
+      kinfo<128, 8, 1, MODE_INNER>("128x8x1"),
+      kinfo<32, 32, 2, MODE_INNER>("32x32x2"),
+      kinfo<32, 32, 1, MODE_INNER>("32x32x1"),
+      kinfo<64, 16, 2, MODE_INNER>("64x16x2"),
+      kinfo<64, 16, 1, MODE_INNER>("64x16x1"),
+      kinfo<32, 16, 2, MODE_INNER>("32x16x2"),
+      kinfo<64, 32, 2, MODE_INNER>("64x32x2"),
+      kinfo<64, 32, 1, MODE_INNER>("64x32x1"),
+      kinfo<128, 16, 1, MODE_INNER>("128x16x1"),
+      kinfo<128, 16, 2, MODE_INNER>("128x16x2"),
+  };
+  *n = (int)(sizeof v / sizeof v[0]);
+  return v;
+}
+
+static KInfo pick_inner() {
+  int n = 0;
+  const KInfo* v = inner_variants(&n);
+  const char* e = getenv("WAVE25_INNER_TILE");
+  if (e)
+    for (int i = 0; i < n; ++i)
+      if (!strcmp(e, v[i].name)) return v[i];
+  return v[0];
+}
 
 enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_N = 3 };
-static const int KTX[KI_N] = {32, 16, 32};
-static const int KTY[KI_N] = {32, 32, 16};
+
+static KInfo g_k[KI_N];
+static void init_kernels() {
+  static bool done = false;
+  if (done) return;
+  g_k[KI_INNER] = pick_inner();
+  g_k[KI_WALLX] = kinfo<16, 32, 2, MODE_WALL>("wallx16x32x2");   // x walls (w wide in x)
+  g_k[KI_WALLY] = kinfo<32, 16, 2, MODE_WALL>("wally32x16x2");   // y walls (w wide in y)
+  done = true;
+}
+#define KTX(ki) (g_k[ki].tx)
+#define KTY(ki) (g_k[ki].ty)
 
 static constexpr double W8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0};
 static constexpr int MAX_W = 512;
@@ -105,6 +149,7 @@ struct wave_plan {
   // launch plans
   Maps maps[KI_N];
   int occ[KI_N] = {1, 1, 1};
+  int pf = 2;                        // L2 prefetch distance (WAVE25_PF), measured best
   std::vector<Launch> launches[3];   // [0] all planes, [1] edges, [2] interior
   // streams / graphs
   cudaStream_t side = nullptr, cap = nullptr;
@@ -210,30 +255,9 @@ static void make_constants(const wave_desc& d, float dt, Coef* k, std::vector<fl
 // ---------------------------------------------------------------------------
 // launch planning
 // ---------------------------------------------------------------------------
-template <int TX, int TY, int TYT, int SU, int SP, int MODE>
-static void* kfn() { return (void*)k_stream<TX, TY, TYT, SU, SP, MODE>; }
-
-static void* kernel_ptr(int ki) {
-  switch (ki) {
-    case KI_INNER: return kfn<INNER_CFG, MODE_INNER>();
-    case KI_WALLX: return kfn<WALLX_CFG, MODE_WALL>();
-    default: return kfn<WALLY_CFG, MODE_WALL>();
-  }
-}
-static int kernel_threads(int ki) {
-  switch (ki) {
-    case KI_INNER: return StreamCfg<INNER_CFG>::NT;
-    case KI_WALLX: return StreamCfg<WALLX_CFG>::NT;
-    default: return StreamCfg<WALLY_CFG>::NT;
-  }
-}
-static size_t kernel_smem(int ki, int w) {
-  switch (ki) {
-    case KI_INNER: return StreamCfg<INNER_CFG>::smem_bytes(w);
-    case KI_WALLX: return StreamCfg<WALLX_CFG>::smem_bytes(w);
-    default: return StreamCfg<WALLY_CFG>::smem_bytes(w);
-  }
-}
+static void* kernel_ptr(int ki) { return g_k[ki].fn; }
+static int kernel_threads(int ki) { return g_k[ki].nt; }
+static size_t kernel_smem(int ki, int w) { return g_k[ki].smem(w); }
 
 // z-chunk length minimising (waves x (chunk + warm-up)) for ncol columns over nz planes
 static int choose_cz(int64_t ncol, int nz, int resident) {
@@ -280,7 +304,7 @@ static wave_status build_launches(wave_plan* P) {
 
 static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 4>>& xy,
                         const std::vector<ZRange>& zr, std::vector<Launch>* out) {
-  const int TX = KTX[ki], TY = KTY[ki];
+  const int TX = KTX(ki), TY = KTY(ki);
   // chunk length from the largest z range and the total column count
   int64_t ncol = 0;
   int nzmax = 0;
@@ -305,6 +329,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   p.k = P->coef;
   p.tab = P->tab_d;
   p.cz = cz;
+  p.pf = P->pf;
   int blk = 0;
   auto flush = [&]() {
     if (p.nreg == 0) return;
@@ -441,7 +466,7 @@ static void drop_graphs(wave_plan* P) {
 // ---------------------------------------------------------------------------
 extern "C" {
 
-const char* wave_version(void) { return "wave25 0.1.0 sm_100a"; }
+const char* wave_version(void) { return "wave25 0.2.0 sm_100a"; }
 
 const char* wave_last_error(void) { return g_err.c_str(); }
 
@@ -511,6 +536,8 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (major != 10) return bail(fail(WAVE_ERR_CUDA, "this library is built for sm_100a (B200); device is sm_%d*", major));
   cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, P->dev);
   if (get_encoder() != WAVE_OK) return bail(WAVE_ERR_CUDA);
+  init_kernels();
+  if (const char* e = getenv("WAVE25_PF")) P->pf = atoi(e);
   const int T = P->d.pml_width + 2;
   if ((e = cudaMalloc(&P->tab_d, 3 * T * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&P->dstep, sizeof(unsigned long long))) != cudaSuccess ||
@@ -570,7 +597,7 @@ wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
   const uint64_t pb = P->L.pitch_x * 4, plb = pb * P->d.ny;
   for (int ki = 0; ki < KI_N; ++ki) {
-    const uint32_t TX = KTX[ki], TY = KTY[ki];
+    const uint32_t TX = KTX(ki), TY = KTY(ki);
     for (int b = 0; b < 2; ++b) {
       CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
       CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX, TY));
