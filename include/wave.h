@@ -247,6 +247,26 @@ WAVE_API float wave_get_dt(const wave_plan *plan);
  * accounting in benchmarks); -1 on NULL. */
 WAVE_API int32_t wave_launches_per_step(const wave_plan *plan);
 
+/* ---- measurement --------------------------------------------------------- */
+
+/* Kernel kinds of one time step (index into the arrays below). */
+enum { WAVE_KK_INTERIOR = 0, WAVE_KK_XWALLS = 1, WAVE_KK_YWALLS = 2, WAVE_KK_SOURCE = 3,
+       WAVE_KK_N = 4 };
+
+/* Points each kernel kind computes per step (interior column incl. z caps,
+ * x walls, y walls, source = 1 if owned), for algorithmic-byte accounting
+ * (16 B per point-step).  out[WAVE_KK_N]. */
+WAVE_API wave_status wave_kernel_points(const wave_plan *plan, int64_t *out);
+
+/* Like wave_step (same kernels, same streams, direct launches instead of the
+ * CUDA graph) but with a CUDA event pair around every kernel launch, each on
+ * the stream that launches it.  Synchronises `stream` at the end and returns
+ * the summed device time of each kernel kind over the nsteps in
+ * kernel_ms[WAVE_KK_N] and the number of launches of each kind in
+ * launches[WAVE_KK_N] (either may be NULL).  Single-slab plans only. */
+WAVE_API wave_status wave_step_profiled(wave_plan *plan, int64_t nsteps, void *stream,
+                                        double *kernel_ms, int64_t *launches);
+
 #ifdef __cplusplus
 }
 #endif

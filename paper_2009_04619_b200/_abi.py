@@ -26,8 +26,10 @@ EXPORTS = [
     "wave_plan_create", "wave_plan_bind", "wave_plan_destroy", "wave_set_velocity",
     "wave_set_source", "wave_set_state", "wave_step", "wave_step_edges", "wave_step_interior",
     "wave_step_finish", "wave_halo_views", "wave_read", "wave_field_ptr", "wave_check_finite",
-    "wave_step_index", "wave_get_dt", "wave_launches_per_step",
+    "wave_step_index", "wave_get_dt", "wave_launches_per_step", "wave_kernel_points",
+    "wave_step_profiled",
 ]
+KERNEL_KINDS = ["interior", "xwalls", "ywalls", "source"]
 
 
 class WaveDesc(ctypes.Structure):
@@ -96,6 +98,8 @@ def lib() -> ctypes.CDLL:
                 "wave_step_index": ([P], i64),
                 "wave_get_dt": ([P], f32),
                 "wave_launches_per_step": ([P], i32),
+                "wave_kernel_points": ([P, P], i32),
+                "wave_step_profiled": ([P, i64, P, P, P], i32),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)
@@ -224,3 +228,19 @@ def wave_get_dt(plan) -> float:
 
 def wave_launches_per_step(plan) -> int:
     return int(lib().wave_launches_per_step(plan))
+
+
+def wave_kernel_points(plan) -> dict:
+    import numpy as np
+    out = np.zeros(4, np.int64)
+    check(lib().wave_kernel_points(plan, out.ctypes.data))
+    return dict(zip(KERNEL_KINDS, (int(v) for v in out)))
+
+
+def wave_step_profiled(plan, nsteps: int, stream: int):
+    """Returns ({kind: summed ms}, {kind: launches}) over nsteps profiled steps."""
+    import numpy as np
+    ms = np.zeros(4, np.float64)
+    n = np.zeros(4, np.int64)
+    check(lib().wave_step_profiled(plan, int(nsteps), stream, ms.ctypes.data, n.ctypes.data))
+    return dict(zip(KERNEL_KINDS, (float(v) for v in ms))), dict(zip(KERNEL_KINDS, (int(v) for v in n)))

@@ -18,12 +18,15 @@
 //    LDS.128 per row; y neighbours: 8 LDS.128 per thread; z: registers.
 //  * All 4*TYT points of a plane are evaluated as interleaved independent
 //    FMA chains; the PML-vs-inner choice is one uniform branch per plane.
-//  * MODE_INNER: region = inner xy footprint over all z; planes in the inner z
-//    range take the inner update; the z-PML caps (global k < w, k >= nz-w)
-//    take the PML update with plane-uniform eta through a non-inlined
-//    function (keeps the hot loop's code small).  MODE_WALL: x/y PML walls,
-//    every point takes the PML update with eta on the 7-point star evaluated
-//    from integer distances (no stored eta array, 0 extra HBM bytes).
+//  * MODE_INNER: region = inner xy footprint over all z; planes inside the
+//    inner z range take the inner update (no per-point branches); the z-PML
+//    caps (global k < w or k >= nz-w) take the PML update with plane-uniform
+//    eta through a non-inlined function (keeps the hot loop's code small).
+//  * MODE_WALL: the x walls (left/right) and y walls (front/back) over all z;
+//    every point takes the PML update.  eta on the 7-point star is evaluated
+//    from integer distances (no stored eta array, 0 extra HBM bytes); its
+//    z-invariant part (grad-eta coefficients, A, B) is precomputed per point
+//    once, and only the planes next to the z caps re-evaluate it in full.
 #pragma once
 #include "common.cuh"
 
@@ -66,10 +69,12 @@ struct StreamCfg {
   static constexpr int BAR_OFF = (SU * U_STAGE + 2 * SP * P_STAGE) * 4;  // bytes
   static constexpr int TAB_OFF = BAR_OFF + (SU + SP) * 8;
   static size_t smem_bytes(int w) { return TAB_OFF + 3 * (w + 2) * 4; }
-  static_assert(TX % 4 == 0 && TY % TYT == 0, "tile shape");
+  static_assert(TX % 32 == 0 && TY % (4 * TYT) == 0, "tile shape: warps are 8 float4 lanes x 4 rows");
   static_assert((U_STAGE * 4) % 128 == 0 && (P_STAGE * 4) % 128 == 0, "TMA smem alignment");
   static_assert(NT % 32 == 0, "whole warps");
 };
+
+struct PmlGeo { int nx, ny, nzg, w, T; float i2hx, i2hy, i2hz; };
 
 // Plane-uniform constants of a z-PML cap plane seen from the inner xy footprint.
 struct CapC { float ex, ezp, ezm, A, B; };
@@ -88,6 +93,49 @@ __device__ __noinline__ float4 cap_update(float4 L, float4 C, float4 up, float4 
     res[c] = upd_pml(f4get(L, c), g, f4get(C, c), f4get(up, c), f4get(v, c), cc.A, cc.B);
   }
   return make_float4(res[0], res[1], res[2], res[3]);
+}
+
+// PML path for one float4 row (4 x-points at gx.., row gy, global plane kg):
+// per point the Chebyshev distance d, eta on the 7-point star from the
+// (w+2)-entry table (eta_{w+1} = 0 outside), the grad-eta . grad-u term and
+// the damped update; points with d = 0 take the inner formula (PAPER.md
+// L320 semantics, identical arithmetic to the naive kernel).
+__device__ __forceinline__ float4 pml_row_impl(float4 L, float4 C, float4 up, float4 v, float4 xp, float4 xm,
+                                               float4 yp, float4 ym, float4 zp, float4 zm, int gx, int gy,
+                                               int kg, const PmlGeo& G, const float* stab) {
+  const int dy = dist1(gy, G.ny, G.w), dyp = dist1(gy + 1, G.ny, G.w), dym = dist1(gy - 1, G.ny, G.w);
+  const int dz = dist1(kg, G.nzg, G.w), dzp = dist1(kg + 1, G.nzg, G.w), dzm = dist1(kg - 1, G.nzg, G.w);
+  int dxs[6];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) dxs[c] = dist1(gx - 1 + c, G.nx, G.w);
+  float res[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int dx = dxs[c + 1];
+    const int dxy = max(dx, dy);
+    const int d = max(dxy, dz);
+    const float uc = f4get(C, c), upc = f4get(up, c), vc = f4get(v, c);
+    const float Lc = f4get(L, c);
+    if (d == 0) {
+      res[c] = upd_inner(Lc, uc, upc, vc);
+    } else {
+      const float exp_ = stab[max(max(dxs[c + 2], dy), dz)], exm = stab[max(max(dxs[c], dy), dz)];
+      const float eyp = stab[max(max(dx, dyp), dz)], eym = stab[max(max(dx, dym), dz)];
+      const float ezp = stab[max(dxy, dzp)], ezm = stab[max(dxy, dzm)];
+      const float g = __fadd_rn(__fadd_rn(gterm(exp_, exm, f4get(xp, c), f4get(xm, c), G.i2hx),
+                                          gterm(eyp, eym, f4get(yp, c), f4get(ym, c), G.i2hy)),
+                                gterm(ezp, ezm, f4get(zp, c), f4get(zm, c), G.i2hz));
+      res[c] = upd_pml(Lc, g, uc, upc, vc, stab[G.T + d], stab[2 * G.T + d]);
+    }
+  }
+  return make_float4(res[0], res[1], res[2], res[3]);
+}
+
+// Out-of-line copy (planes next to the z caps in the wall kernel).
+__device__ __noinline__ float4 pml_row_call(float4 L, float4 C, float4 up, float4 v, float4 xp, float4 xm,
+                                            float4 yp, float4 ym, float4 zp, float4 zm, int gx, int gy, int kg,
+                                            PmlGeo G, const float* stab) {
+  return pml_row_impl(L, C, up, v, xp, xm, yp, ym, zp, zm, gx, gy, kg, G, stab);
 }
 
 template <int TX, int TY, int TYT, int MODE>
@@ -123,8 +171,10 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
   const int ze = min(zs + P.cz, G.z1);
 
   const int tid = threadIdx.x;
-  const int lx = tid % C::LX;
-  const int ly = tid / C::LX;
+  constexpr int WX = TX / 32;               // warps across x; a warp = 8 float4 lanes x 4 rows
+  const int lane = tid & 31, wid = tid >> 5;
+  const int lx = (wid % WX) * 8 + (lane & 7);
+  const int ly = (wid / WX) * 4 + (lane >> 3);
   const int gx = tx0 + 4 * lx;              // first x of my float4
   const int gy = ty0 + ly * TYT;            // first y of my rows
   // smem offsets (floats) of my float4 in row 0 of the tile, u stage / p stage
@@ -175,8 +225,12 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
       if (x >= G.x0 && x < G.x1 && y >= G.y0 && y < G.y1) mask |= 1u << (r * 4 + c);
     }
   const bool full = mask == (TYT * 4 == 32 ? 0xffffffffu : ((1u << (TYT * 4)) - 1u));
-  // wall mode: z-independent parts of the 7-point eta star per point
-  int dxy[TYT][4], ixp[TYT][4], ixm[TYT][4], iyp[TYT][4], iym[TYT][4];
+  PmlGeo PG;
+  PG.nx = P.nx; PG.ny = P.ny; PG.nzg = P.nzg; PG.w = P.w; PG.T = TABN;
+  PG.i2hx = P.k.i2h[0]; PG.i2hy = P.k.i2h[1]; PG.i2hz = P.k.i2h[2];
+  // wall mode: z-invariant PML coefficients of my points, valid on planes with
+  // dz(k-1) = dz(k) = dz(k+1) = 0:  cg_a = (eta(+e_a) - eta(-e_a)) / (2 h_a), A_d, B_d
+  float cgx[TYT][4], cgy[TYT][4], A0[TYT][4], B0[TYT][4];
   if (MODE == MODE_WALL) {
 #pragma unroll
     for (int r = 0; r < TYT; ++r) {
@@ -185,11 +239,12 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int dx = dist1(gx + c, P.nx, P.w);
-        dxy[r][c] = max(dx, dy);
-        ixp[r][c] = max(dist1(gx + c + 1, P.nx, P.w), dy);
-        ixm[r][c] = max(dist1(gx + c - 1, P.nx, P.w), dy);
-        iyp[r][c] = max(dx, dyp);
-        iym[r][c] = max(dx, dym);
+        const int d0 = max(dx, dy);
+        cgx[r][c] = __fmul_rn(__fsub_rn(stab[max(dist1(gx + c + 1, P.nx, P.w), dy)],
+                                        stab[max(dist1(gx + c - 1, P.nx, P.w), dy)]), PG.i2hx);
+        cgy[r][c] = __fmul_rn(__fsub_rn(stab[max(dx, dyp)], stab[max(dx, dym)]), PG.i2hy);
+        A0[r][c] = stab[TABN + d0];
+        B0[r][c] = stab[2 * TABN + d0];
       }
     }
   }
@@ -313,9 +368,9 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
                                 K.i2h[0], K.i2h[1], K.i2h[2]);
           }
         }
-      } else {
-        const int dzk = dist1(kg, P.nzg, P.w);
-        const int dzp = dist1(kg + 1, P.nzg, P.w), dzm = dist1(kg - 1, P.nzg, P.w);
+      } else if (kg > P.w && kg < P.nzg - P.w - 1) {
+        // wall, z-interior plane: eta star is z-invariant (dz = 0 at k-1, k, k+1);
+        // g = gx + gy (+ gz = +-0 exactly, dropped)
 #pragma unroll
         for (int r = 0; r < TYT; ++r) {
           const float4 Cu = Y[R + r];
@@ -324,18 +379,24 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
           float o[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const int d = max(dxy[r][c], dzk);
-            const float exp_ = stab[max(ixp[r][c], dzk)], exm = stab[max(ixm[r][c], dzk)];
-            const float eyp = stab[max(iyp[r][c], dzk)], eym = stab[max(iym[r][c], dzk)];
-            const float ezp = stab[max(dxy[r][c], dzp)], ezm = stab[max(dxy[r][c], dzm)];
-            const float g = __fadd_rn(
-                __fadd_rn(gterm(exp_, exm, X[5 + c], X[3 + c], K.i2h[0]),
-                          gterm(eyp, eym, f4get(Y[R + r + 1], c), f4get(Y[R + r - 1], c), K.i2h[1])),
-                gterm(ezp, ezm, f4get(q[(s + 5) % 9][r], c), f4get(q[(s + 3) % 9][r], c), K.i2h[2]));
-            o[c] = upd_pml(L[r][c], g, X[4 + c], f4get(upv[r], c), f4get(vv[r], c), stab[TABN + d],
-                           stab[2 * TABN + d]);
+            const float gxa = __fmul_rn(cgx[r][c], __fmul_rn(__fsub_rn(X[5 + c], X[3 + c]), K.i2h[0]));
+            const float gya = __fmul_rn(cgy[r][c], __fmul_rn(__fsub_rn(f4get(Y[R + r + 1], c),
+                                                                       f4get(Y[R + r - 1], c)), K.i2h[1]));
+            o[c] = upd_pml(L[r][c], __fadd_rn(gxa, gya), X[4 + c], f4get(upv[r], c), f4get(vv[r], c),
+                           A0[r][c], B0[r][c]);
           }
           res[r] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+      } else {
+        // wall, plane in or next to a z cap: full 7-point eta star per point
+#pragma unroll
+        for (int r = 0; r < TYT; ++r) {
+          const float4 Cu = Y[R + r];
+          const float4 xp = make_float4(Cu.y, Cu.z, Cu.w, Rf[r].x);
+          const float4 xm = make_float4(Lf[r].w, Cu.x, Cu.y, Cu.z);
+          res[r] = pml_row_call(make_float4(L[r][0], L[r][1], L[r][2], L[r][3]), Cu, upv[r], vv[r], xp, xm,
+                                Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], gx, gy + r,
+                                kg, PG, stab);
         }
       }
       if (full) {

@@ -67,28 +67,39 @@ static KInfo kinfo(const char* name) {
                &StreamCfg<TX, TY, TYT>::smem_bytes, name};
 }
 
-// interior-column variants (WAVE25_INNER_TILE selects one; default first)
+// interior-kernel variants (WAVE25_INNER_TILE selects one; default first)
 static const KInfo* inner_variants(int* n) {
   static const KInfo v[] = {
       kinfo<128, 8, 1, MODE_INNER>("128x8x1"),
-      kinfo<32, 32, 2, MODE_INNER>("32x32x2"),
-      kinfo<32, 32, 1, MODE_INNER>("32x32x1"),
-      kinfo<64, 16, 2, MODE_INNER>("64x16x2"),
       kinfo<64, 16, 1, MODE_INNER>("64x16x1"),
-      kinfo<32, 16, 2, MODE_INNER>("32x16x2"),
-      kinfo<64, 32, 2, MODE_INNER>("64x32x2"),
-      kinfo<64, 32, 1, MODE_INNER>("64x32x1"),
       kinfo<128, 16, 1, MODE_INNER>("128x16x1"),
-      kinfo<128, 16, 2, MODE_INNER>("128x16x2"),
+      kinfo<64, 32, 2, MODE_INNER>("64x32x2"),
   };
   *n = (int)(sizeof v / sizeof v[0]);
   return v;
 }
 
-static KInfo pick_inner() {
-  int n = 0;
-  const KInfo* v = inner_variants(&n);
-  const char* e = getenv("WAVE25_INNER_TILE");
+static const KInfo* wallx_variants(int* n) {
+  static const KInfo v[] = {
+      kinfo<32, 32, 1, MODE_WALL>("x32x32x1"),
+      kinfo<32, 64, 2, MODE_WALL>("x32x64x2"),
+      kinfo<32, 16, 1, MODE_WALL>("x32x16x1"),
+  };
+  *n = (int)(sizeof v / sizeof v[0]);
+  return v;
+}
+
+static const KInfo* wally_variants(int* n) {
+  static const KInfo v[] = {
+      kinfo<128, 16, 1, MODE_WALL>("y128x16x1"),
+      kinfo<64, 16, 1, MODE_WALL>("y64x16x1"),
+  };
+  *n = (int)(sizeof v / sizeof v[0]);
+  return v;
+}
+
+static KInfo pick(const KInfo* v, int n, const char* env) {
+  const char* e = getenv(env);
   if (e)
     for (int i = 0; i < n; ++i)
       if (!strcmp(e, v[i].name)) return v[i];
@@ -101,9 +112,13 @@ static KInfo g_k[KI_N];
 static void init_kernels() {
   static bool done = false;
   if (done) return;
-  g_k[KI_INNER] = pick_inner();
-  g_k[KI_WALLX] = kinfo<16, 32, 2, MODE_WALL>("wallx16x32x2");   // x walls (w wide in x)
-  g_k[KI_WALLY] = kinfo<32, 16, 2, MODE_WALL>("wally32x16x2");   // y walls (w wide in y)
+  int n = 0;
+  const KInfo* v = inner_variants(&n);
+  g_k[KI_INNER] = pick(v, n, "WAVE25_INNER_TILE");
+  v = wallx_variants(&n);
+  g_k[KI_WALLX] = pick(v, n, "WAVE25_WALLX_TILE");
+  v = wally_variants(&n);
+  g_k[KI_WALLY] = pick(v, n, "WAVE25_WALLY_TILE");
   done = true;
 }
 #define KTX(ki) (g_k[ki].tx)
@@ -259,6 +274,14 @@ static void* kernel_ptr(int ki) { return g_k[ki].fn; }
 static int kernel_threads(int ki) { return g_k[ki].nt; }
 static size_t kernel_smem(int ki, int w) { return g_k[ki].smem(w); }
 
+// x origin of a region's first tile: 4-aligned (float4 stores); a region
+// narrower than one tile (a thin x wall) gets a single tile ending at x1 so its
+// rows are whole TX-float segments (DRAM-friendly) instead of starting mid-row.
+static int tile_origin(int x0, int x1, int TX) {
+  if (x1 - x0 <= TX && x1 - TX >= 0) return std::min(x0, x1 - TX) & ~3;
+  return x0 & ~3;
+}
+
 // z-chunk length minimising (waves x (chunk + warm-up)) for ncol columns over nz planes
 static int choose_cz(int64_t ncol, int nz, int resident) {
   int best = nz;
@@ -293,7 +316,9 @@ static wave_status build_launches(wave_plan* P) {
   for (int s = 0; s < 3; ++s) {
     P->launches[s].clear();
     if (sets[s]->empty()) continue;
+    // interior kernel: inner xy footprint, all z (z caps plane-uniform)
     add_regions(P, KI_INNER, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
+    // boundary kernels: left/right (x) walls; front/back (y) walls over full x
     if (w > 0) {
       add_regions(P, KI_WALLX, {{0, w, w, ny - w}, {nx - w, nx, w, ny - w}}, *sets[s], &P->launches[s]);
       add_regions(P, KI_WALLY, {{0, nx, 0, w}, {0, nx, ny - w, ny}}, *sets[s], &P->launches[s]);
@@ -310,7 +335,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   int nzmax = 0;
   for (auto& b : xy) {
     if (b[1] <= b[0] || b[3] <= b[2]) continue;
-    const int ax0 = b[0] & ~3;
+    const int ax0 = tile_origin(b[0], b[1], TX);
     ncol += (int64_t)((b[1] - ax0 + TX - 1) / TX) * ((b[3] - b[2] + TY - 1) / TY);
   }
   for (auto& z : zr) nzmax = std::max(nzmax, z.z1 - z.z0);
@@ -344,7 +369,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
       if (p.nreg == MAX_REGIONS) flush();
       Region& g = p.reg[p.nreg++];
       g.x0 = b[0]; g.x1 = b[1]; g.y0 = b[2]; g.y1 = b[3]; g.z0 = z.z0; g.z1 = z.z1;
-      g.ax0 = b[0] & ~3;
+      g.ax0 = tile_origin(b[0], b[1], TX);
       g.ntx = (b[1] - g.ax0 + TX - 1) / TX;
       g.nty = (b[3] - b[2] + TY - 1) / TY;
       g.nzc = (z.z1 - z.z0 + cz - 1) / cz;
@@ -407,7 +432,7 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, cudaStream_
   }
   const std::vector<Launch>& Ls = P->launches[which];
   if (Ls.empty()) return WAVE_OK;
-  // fork: the first launch (interior column) on s, the walls on the side stream
+  // fork: the interior kernel on s, the wall kernels on the side stream
   bool forked = false;
   for (size_t i = 0; i < Ls.size(); ++i) {
     if (Ls[i].ki == KI_INNER || Ls.size() == 1) {
@@ -808,6 +833,82 @@ wave_status wave_check_finite(wave_plan* P, float* h_maxabs, void* stream) {
 int64_t wave_step_index(const wave_plan* P) { return P ? P->step : -1; }
 
 float wave_get_dt(const wave_plan* P) { return P ? P->dt : 0.f; }
+
+wave_status wave_kernel_points(const wave_plan* P, int64_t* out) {
+  if (!P || !out) return fail(WAVE_ERR_CONFIG, "bad arguments");
+  for (int k = 0; k < WAVE_KK_N; ++k) out[k] = 0;
+  for (const Launch& L : P->launches[0])
+    for (int r = 0; r < L.p.nreg; ++r) {
+      const Region& g = L.p.reg[r];
+      out[L.ki] += (int64_t)(g.x1 - g.x0) * (g.y1 - g.y0) * (g.z1 - g.z0);
+    }
+  out[WAVE_KK_SOURCE] = (P->src_set && P->src_local && P->ninc > 0) ? 1 : 0;
+  return WAVE_OK;
+}
+
+wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, double* kernel_ms, int64_t* launches) {
+  CKST(ready(P));
+  if (nsteps < 0) return fail(WAVE_ERR_CONFIG, "nsteps < 0");
+  if (P->d.nz != P->d.nz_global) return fail(WAVE_ERR_STATE, "multi-slab plan: use the split-step calls");
+  if (P->d.kernel != WAVE_KERNEL_STREAM) return fail(WAVE_ERR_STATE, "profiling needs the stream kernels");
+  cudaStream_t s = (cudaStream_t)stream;
+  struct Rec { int kind; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  auto mk = [&](int kind, cudaStream_t st) -> wave_status {
+    Rec r{kind, nullptr, nullptr};
+    CK(cudaEventCreate(&r.a));
+    CK(cudaEventCreate(&r.b));
+    CK(cudaEventRecord(r.a, st));
+    recs.push_back(r);
+    return WAVE_OK;
+  };
+  wave_status st = WAVE_OK;
+  for (int64_t n = 0; n < nsteps && st == WAVE_OK; ++n) {
+    const int cur = P->cur;
+    bool forked = false;
+    for (const Launch& L : P->launches[0]) {
+      cudaStream_t ls = s;
+      if (L.ki != KI_INNER) {
+        if (!forked) {
+          CK(cudaEventRecord(P->ev_fork, s));
+          CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
+          forked = true;
+        }
+        ls = P->side;
+      }
+      CKST(mk(L.ki, ls));
+      CKST(launch_stream(P, L, cur, ls));
+      CK(cudaEventRecord(recs.back().b, ls));
+    }
+    if (forked) {
+      CK(cudaEventRecord(P->ev_join, P->side));
+      CK(cudaStreamWaitEvent(s, P->ev_join, 0));
+    }
+    if (P->src_set && P->src_local && P->ninc > 0) {
+      CKST(mk(WAVE_KK_SOURCE, s));
+      CKST(launch_source(P, cur, s));
+      CK(cudaEventRecord(recs.back().b, s));
+    }
+    P->cur = 1 - P->cur;
+    P->step += 1;
+  }
+  CK(cudaStreamSynchronize(s));
+  double ms[WAVE_KK_N] = {0, 0, 0, 0};
+  int64_t cnt[WAVE_KK_N] = {0, 0, 0, 0};
+  for (Rec& r : recs) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.kind] += t;
+    cnt[r.kind] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (int k = 0; k < WAVE_KK_N; ++k) {
+    if (kernel_ms) kernel_ms[k] = ms[k];
+    if (launches) launches[k] = cnt[k];
+  }
+  return WAVE_OK;
+}
 
 int32_t wave_launches_per_step(const wave_plan* P) {
   if (!P) return -1;

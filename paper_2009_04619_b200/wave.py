@@ -156,6 +156,15 @@ class WavePlan:
     def launches_per_step(self) -> int:
         return _abi.wave_launches_per_step(self._plan)
 
+    def kernel_points(self) -> dict:
+        return _abi.wave_kernel_points(self._plan)
+
+    def step_profiled(self, n: int, stream=None):
+        """n steps with a CUDA event pair around every kernel launch (each on
+        its launching stream); returns ({kind: ms summed}, {kind: launches})."""
+        with torch.cuda.device(self.device):
+            return _abi.wave_step_profiled(self._plan, n, _stream_handle(stream))
+
     def close(self) -> None:
         if self._plan is not None:
             torch.cuda.synchronize(self.device)
