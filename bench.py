@@ -256,11 +256,16 @@ def run_ours(args, rank, world, local):
     from paper_2009_04619_b200.dist import SlabRunner, slab_bounds
 
     __graft_entry__.build_cuda()
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("WAVE25_DIST_BACKEND", "nccl")   # gloo: smoke-test on 1 GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     s, desc = workload(args.config, world)
     off, nzl = slab_bounds(s.nz, rank, world) if world > 1 else (0, s.nz)
     V = synth.velocity(s, nz_global=s.nz, z_offset=off, nz_local=nzl)
@@ -269,20 +274,25 @@ def run_ours(args, rank, world, local):
 
     def barrier():
         if dist is not None:
-            dist.barrier(device_ids=[local])
+            if dist.get_backend() == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize()
 
     def maxall(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     plan = WavePlan(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
     plan.set_velocity(V)
     plan.set_source(*s.source, wl)
-    runner = SlabRunner(plan, rank, world) if world > 1 else None
+    runner = (SlabRunner(plan, rank, world, stage_on_host=os.environ.get("WAVE25_DIST_BACKEND", "nccl") != "nccl")
+              if world > 1 else None)
     stream = torch.cuda.current_stream()
 
     def steps(n):

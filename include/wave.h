@@ -211,13 +211,15 @@ WAVE_API wave_status wave_step_edges(wave_plan *plan, void *stream);
 WAVE_API wave_status wave_step_interior(wave_plan *plan, void *stream);
 WAVE_API wave_status wave_step_finish(wave_plan *plan);
 
-/* Device pointers, into the buffer that wave_step_edges writes (the next
- * u^n), of the 4-plane blocks to SEND to the lower / upper neighbour (local
- * planes [0,4) and [nz-4,nz)) and of the ghost blocks to RECEIVE into (the 4
- * planes below / above the slab).  Each block is *count contiguous floats.
- * Valid between wave_step_edges and wave_step_finish. */
-WAVE_API wave_status wave_halo_views(const wave_plan *plan, float **send_lo, float **send_hi,
-                            float **recv_lo, float **recv_hi, int64_t *count);
+/* Device pointers of the 4-plane blocks to SEND to the lower / upper
+ * neighbour (local planes [0,4) and [nz-4,nz)) and of the ghost blocks to
+ * RECEIVE into (the 4 planes below / above the slab); each block is *count
+ * contiguous floats.  which = 0: in the buffer wave_step_edges writes (the
+ * next u^n; valid between wave_step_edges and wave_step_finish); which = 1:
+ * in the current u^n (for the initial halo of a non-zero starting state). */
+WAVE_API wave_status wave_halo_views(const wave_plan *plan, int32_t which, float **send_lo,
+                                     float **send_hi, float **recv_lo, float **recv_hi,
+                                     int64_t *count);
 
 /* ---- outputs ------------------------------------------------------------- */
 

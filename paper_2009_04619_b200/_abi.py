@@ -90,7 +90,7 @@ def lib() -> ctypes.CDLL:
                 "wave_step_edges": ([P, P], i32),
                 "wave_step_interior": ([P, P], i32),
                 "wave_step_finish": ([P], i32),
-                "wave_halo_views": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
+                "wave_halo_views": ([P, i32, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
                                      ctypes.POINTER(P), ctypes.POINTER(i64)], i32),
                 "wave_read": ([P, i32, P, i32, P], i32),
                 "wave_field_ptr": ([P, i32, ctypes.POINTER(P)], i32),
@@ -194,10 +194,10 @@ def wave_step_finish(plan) -> None:
     check(lib().wave_step_finish(plan))
 
 
-def wave_halo_views(plan):
+def wave_halo_views(plan, which: int = 0):
     a, b, c, d = (ctypes.c_void_p() for _ in range(4))
     n = ctypes.c_int64()
-    check(lib().wave_halo_views(plan, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+    check(lib().wave_halo_views(plan, int(which), ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                                 ctypes.byref(d), ctypes.byref(n)))
     return a.value, b.value, c.value, d.value, n.value
 

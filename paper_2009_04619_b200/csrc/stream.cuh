@@ -1,23 +1,25 @@
 // stream.cuh -- the z-streaming stencil kernel for sm_100a (interior column
 // and PML walls).  Design:
 //
-//  * Work unit = one TX x TY xy-tile of one region x one z-chunk [zs, ze).
-//    Blocks are ordered chunk-major (all tiles of chunk 0, then chunk 1, ...)
-//    so co-resident CTAs are xy-neighbours at similar z and the 4-cell halo
-//    rows they re-read come from L2, not HBM.
-//  * u planes (tile + 4-cell halo, (TX+8) x (TY+8) floats) arrive by TMA
-//    (cp.async.bulk.tensor.3d) into a 9-stage shared-memory ring, one mbarrier
-//    per stage; out-of-bounds x/y cells are zero-filled by TMA, so the
-//    Dirichlet fringe costs nothing.  u_prev and vdt2 planes (tile only)
-//    arrive the same way into a 3-stage ring.  9 = the z-window 2R+1, so with
-//    the plane loop unrolled 9x every stage index, register-queue slot and
-//    mbarrier parity is a compile-time constant (no address arithmetic).
-//  * Each thread owns 4 consecutive x points (one float4) x TYT rows and keeps
-//    u(z-4..z+4) of its points in a 9-slot register queue with fixed slots --
-//    the paper's st_reg_fixed idea.  x neighbours: 2
-//    LDS.128 per row; y neighbours: 8 LDS.128 per thread; z: registers.
-//  * All 4*TYT points of a plane are evaluated as interleaved independent
-//    FMA chains; the PML-vs-inner choice is one uniform branch per plane.
+//  * Work unit = one CW x TY xy-tile (CW = computed width) of one region x one
+//    z-chunk [zs, ze).  Blocks are ordered chunk-major (all tiles of chunk 0,
+//    then chunk 1, ...) so co-resident CTAs are xy-neighbours at similar z and
+//    the 4-cell halo rows they re-read come from L2, not HBM.
+//  * A producer warp streams, by TMA (cp.async.bulk.tensor.3d), u planes of a
+//    TX-wide box + 4-cell halo ((TX+8) x (TY+8) floats, TX >= CW, 128-B
+//    aligned where possible) into a 9-stage shared-memory ring and u_prev /
+//    vdt2 tiles (CW x TY) into a 3-stage ring; full/empty mbarrier pairs per
+//    stage (Blackwell producer/consumer pipeline, no block-wide barrier in the
+//    loop).  Out-of-bounds x/y cells are zero-filled by TMA, so the Dirichlet
+//    fringe costs nothing.  An L2 tensor prefetch runs P.pf planes ahead.
+//    9 = the z-window 2R+1, so with the plane loop unrolled 9x every stage
+//    index, register-queue slot and mbarrier parity is a compile-time constant.
+//  * Each consumer thread owns 4 consecutive x points (one float4) x TYT rows
+//    and keeps u(z-4..z+4) of its points in a 9-slot register queue with fixed
+//    slots -- the paper's st_reg_fixed idea.  x neighbours:
+//    2 LDS.128 per row; y neighbours: 8 LDS.128 per thread; z: registers.
+//  * All 4*TYT points of a plane are evaluated as interleaved independent FMA
+//    chains; the PML-vs-inner choice is one uniform branch per plane.
 //  * MODE_INNER: region = inner xy footprint over all z; planes inside the
 //    inner z range take the inner update (no per-point branches); the z-PML
 //    caps (global k < w or k >= nz-w) take the PML update with plane-uniform
@@ -32,12 +34,14 @@
 
 namespace w25 {
 
-enum { MODE_INNER = 0, MODE_WALL = 1 };
+// MODE_FUSED: whole xy plane in one launch, path chosen per warp and plane.
+// MODE_NULL: memory-pattern probe (no stencil; wrong results, diagnostics only).
+enum { MODE_INNER = 0, MODE_WALL = 1, MODE_NULL = 2, MODE_FUSED = 3 };
 
 struct Region {
   int x0, x1, y0, y1, z0, z1;   // point box [x0,x1) x [y0,y1) x [z0,z1) (local z)
-  int ax0;                      // x0 rounded down to a multiple of 4 (tile origin)
-  int ntx, nty, nzc;            // tiles in x, y and z-chunks
+  int ax0;                      // x0 rounded down to a multiple of 4 (first computed column)
+  int ntx, nty, nzc;            // tiles in x (step CW), y (step TY) and z-chunks
   int blk0;                     // first blockIdx.x of this region
 };
 
@@ -50,28 +54,38 @@ struct StreamParams {
   int64_t pitch, plane;         // row / plane pitch in floats
   int nx, ny, nzl, nzg, zoff, w;
   int cz;                       // z-chunk length
-  int pf;                       // L2 prefetch distance (planes beyond the TMA rings; 0 = off)
+  int pf;                       // L2 prefetch distance (planes beyond the rings; 0 = off)
+  int order;                    // tile order in a chunk: 0 = x fastest; G > 0 = groups of G x-tiles, y inside
+  int upol;                     // L2 policy of u loads: 0 = evict_last, 1 = evict_normal
   int nreg;
   Region reg[MAX_REGIONS];
   Coef k;
   const float* tab;             // [3][w+2]: eta_d, A_d, B_d (d = 0..w), eta_{w+1} = 0
 };
 
-template <int TX, int TY, int TYT>
+template <int TX, int CW, int TY, int TYT, int MINB = 2>
 struct StreamCfg {
-  static constexpr int LX = TX / 4;               // float4 lanes across x
-  static constexpr int LY = TY / TYT;             // thread rows
-  static constexpr int NT = LX * LY;              // threads per CTA
-  static constexpr int SW = TX + 2 * R;           // smem u row stride (floats)
+  static constexpr int LXW = (CW / 4) < 8 ? (CW / 4) : 8;   // float4 lanes per warp row
+  static constexpr int LYW = 32 / LXW;                      // thread rows per warp
+  static constexpr int WX = (CW / 4) / LXW;                 // consumer warps across x
+  static constexpr int WY = (TY / TYT) / LYW;               // consumer warps in y
+  static constexpr int NWC = WX * WY;                       // consumer warps
+  static constexpr int NT = 32 * (NWC + 1);                 // + 1 producer warp
+  // register cap for MINB CTAs per SM: warps are placed round-robin on the 4
+  // sub-partitions, each with a 16K-register file
+  static constexpr int WPS = (MINB * (NWC + 1) + 3) / 4;   // warps per sub-partition
+  static constexpr int MAXR_ = (16384 / (32 * WPS)) & ~7;
+  static constexpr int MAXR = MAXR_ > 255 ? 255 : MAXR_;
+  static constexpr int SW = TX + 2 * R;                     // smem u row stride (floats)
   static constexpr int SH = TY + 2 * R;
-  static constexpr int U_STAGE = SW * SH;         // floats per u stage
-  static constexpr int P_STAGE = TX * TY;         // floats per u_prev / vdt2 stage
+  static constexpr int U_STAGE = SW * SH;                   // floats per u stage
+  static constexpr int P_STAGE = CW * TY;                   // floats per u_prev / vdt2 stage
   static constexpr int BAR_OFF = (SU * U_STAGE + 2 * SP * P_STAGE) * 4;  // bytes
-  static constexpr int TAB_OFF = BAR_OFF + (SU + SP) * 8;
+  static constexpr int TAB_OFF = BAR_OFF + 2 * (SU + SP) * 8;
   static size_t smem_bytes(int w) { return TAB_OFF + 3 * (w + 2) * 4; }
-  static_assert(TX % 32 == 0 && TY % (4 * TYT) == 0, "tile shape: warps are 8 float4 lanes x 4 rows");
+  static_assert(CW % 4 == 0 && CW <= TX && TX % 4 == 0, "tile widths");
+  static_assert(32 % LXW == 0 && (TY / TYT) % LYW == 0 && TY % TYT == 0, "warp tiling");
   static_assert((U_STAGE * 4) % 128 == 0 && (P_STAGE * 4) % 128 == 0, "TMA smem alignment");
-  static_assert(NT % 32 == 0, "whole warps");
 };
 
 struct PmlGeo { int nx, ny, nzg, w, T; float i2hx, i2hy, i2hz; };
@@ -98,11 +112,11 @@ __device__ __noinline__ float4 cap_update(float4 L, float4 C, float4 up, float4 
 // PML path for one float4 row (4 x-points at gx.., row gy, global plane kg):
 // per point the Chebyshev distance d, eta on the 7-point star from the
 // (w+2)-entry table (eta_{w+1} = 0 outside), the grad-eta . grad-u term and
-// the damped update; points with d = 0 take the inner formula (PAPER.md
-// L320 semantics, identical arithmetic to the naive kernel).
-__device__ __forceinline__ float4 pml_row_impl(float4 L, float4 C, float4 up, float4 v, float4 xp, float4 xm,
-                                               float4 yp, float4 ym, float4 zp, float4 zm, int gx, int gy,
-                                               int kg, const PmlGeo& G, const float* stab) {
+// the damped update; points with d = 0 take the inner formula (identical
+// arithmetic to the naive kernel).  Used for wall planes in / next to a cap.
+__device__ __noinline__ float4 pml_row_call(float4 L, float4 C, float4 up, float4 v, float4 xp, float4 xm,
+                                            float4 yp, float4 ym, float4 zp, float4 zm, int gx, int gy, int kg,
+                                            PmlGeo G, const float* stab) {
   const int dy = dist1(gy, G.ny, G.w), dyp = dist1(gy + 1, G.ny, G.w), dym = dist1(gy - 1, G.ny, G.w);
   const int dz = dist1(kg, G.nzg, G.w), dzp = dist1(kg + 1, G.nzg, G.w), dzm = dist1(kg - 1, G.nzg, G.w);
   int dxs[6];
@@ -131,26 +145,21 @@ __device__ __forceinline__ float4 pml_row_impl(float4 L, float4 C, float4 up, fl
   return make_float4(res[0], res[1], res[2], res[3]);
 }
 
-// Out-of-line copy (planes next to the z caps in the wall kernel).
-__device__ __noinline__ float4 pml_row_call(float4 L, float4 C, float4 up, float4 v, float4 xp, float4 xm,
-                                            float4 yp, float4 ym, float4 zp, float4 zm, int gx, int gy, int kg,
-                                            PmlGeo G, const float* stab) {
-  return pml_row_impl(L, C, up, v, xp, xm, yp, ym, zp, zm, gx, gy, kg, G, stab);
-}
-
-template <int TX, int TY, int TYT, int MODE>
-__global__ void __launch_bounds__(StreamCfg<TX, TY, TYT>::NT)
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB>
+__global__ void __maxnreg__((StreamCfg<TX, CW, TY, TYT, MINB>::MAXR))
 k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1)
-         const __grid_constant__ CUtensorMap tm_up,   // u^{n-1}, box (TX, TY, 1)
-         const __grid_constant__ CUtensorMap tm_v,    // vdt2, box (TX, TY, 1)
+         const __grid_constant__ CUtensorMap tm_up,   // u^{n-1}, box (CW, TY, 1)
+         const __grid_constant__ CUtensorMap tm_v,    // vdt2, box (CW, TY, 1)
          const __grid_constant__ StreamParams P) {
-  using C = StreamCfg<TX, TY, TYT>;
+  using C = StreamCfg<TX, CW, TY, TYT, MINB>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* su = reinterpret_cast<float*>(smem_raw);
   float* sup = su + SU * C::U_STAGE;
   float* sv = sup + SP * C::P_STAGE;
-  uint64_t* bar_u = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF);
-  uint64_t* bar_p = bar_u + SU;
+  uint64_t* full_u = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF);
+  uint64_t* empty_u = full_u + SU;
+  uint64_t* full_p = empty_u + SU;
+  uint64_t* empty_p = full_p + SP;
   float* stab = reinterpret_cast<float*>(smem_raw + C::TAB_OFF);
   const int TABN = P.w + 2;
 
@@ -163,59 +172,96 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
   const int ncol = G.ntx * G.nty;
   const int zc = b / ncol;
   const int rem = b - zc * ncol;
-  const int tyi = rem / G.ntx;
-  const int txi = rem - tyi * G.ntx;
-  const int tx0 = G.ax0 + txi * TX;
+  int tyi, txi;
+  if (P.order <= 0) {
+    tyi = rem / G.ntx;
+    txi = rem - tyi * G.ntx;
+  } else {                                 // groups of P.order x-tiles; inside a group y-major
+    const int grp = rem / (P.order * G.nty);
+    const int gsz = min(P.order, G.ntx - grp * P.order);
+    const int r2 = rem - grp * P.order * G.nty;
+    tyi = r2 / gsz;
+    txi = grp * P.order + (r2 - tyi * gsz);
+  }
+  const int cx0 = G.ax0 + txi * CW;                       // first computed column
+  const int cxo = min(((cx0 % TX) + TX) % TX, TX - CW);   // its offset inside the TX-wide box
+  const int bx0 = cx0 - cxo;                              // box origin (128-B aligned when possible)
   const int ty0 = G.y0 + tyi * TY;
   const int zs = G.z0 + zc * P.cz;
   const int ze = min(zs + P.cz, G.z1);
 
   const int tid = threadIdx.x;
-  constexpr int WX = TX / 32;               // warps across x; a warp = 8 float4 lanes x 4 rows
   const int lane = tid & 31, wid = tid >> 5;
-  const int lx = (wid % WX) * 8 + (lane & 7);
-  const int ly = (wid / WX) * 4 + (lane >> 3);
-  const int gx = tx0 + 4 * lx;              // first x of my float4
-  const int gy = ty0 + ly * TYT;            // first y of my rows
-  // smem offsets (floats) of my float4 in row 0 of the tile, u stage / p stage
-  const int uo = (ly * TYT + R) * C::SW + 4 * lx + R;
-  const int po = (ly * TYT) * TX + 4 * lx;
 
-  // ---- setup: barriers, PML tables, prologue TMA ------------------------
+  // ---- setup: barriers, PML tables --------------------------------------
   if (tid == 0) {
     prefetch_tmap(&tm_u);
     prefetch_tmap(&tm_up);
     prefetch_tmap(&tm_v);
 #pragma unroll
-    for (int s = 0; s < SU; ++s) mbar_init(&bar_u[s], 1);
+    for (int s = 0; s < SU; ++s) { mbar_init(&full_u[s], 1); mbar_init(&empty_u[s], C::NWC); }
 #pragma unroll
-    for (int s = 0; s < SP; ++s) mbar_init(&bar_p[s], 1);
+    for (int s = 0; s < SP; ++s) { mbar_init(&full_p[s], 1); mbar_init(&empty_p[s], C::NWC); }
     fence_mbar_init();
   }
   for (int i = tid; i < 3 * TABN; i += C::NT) stab[i] = P.tab[i];
   __syncthreads();
 
-  const uint64_t pol_u = policy_evict_last();    // u^n: re-read (halo) by neighbours
-  const uint64_t pol_s = policy_evict_first();   // u^{n-1}, vdt2: streamed once
-  // plane p (local z, p >= zs-4) lives in u stage (p - zs + 4) % 9
-  auto issue_u = [&](int p, int s) {
-    mbar_arrive_expect_tx(&bar_u[s], C::U_STAGE * 4);
-    tma_load_3d(su + s * C::U_STAGE, &tm_u, &bar_u[s], tx0 - R, ty0 - R, p + R, pol_u);
-  };
-  // plane p (p >= zs) lives in p stage (p - zs) % 3
-  auto issue_p = [&](int p, int s) {
-    mbar_arrive_expect_tx(&bar_p[s], 2 * C::P_STAGE * 4);
-    tma_load_3d(sup + s * C::P_STAGE, &tm_up, &bar_p[s], tx0, ty0, p + R, pol_s);
-    tma_load_3d(sv + s * C::P_STAGE, &tm_v, &bar_p[s], tx0, ty0, p, pol_s);
-  };
-  if (tid == 0) {
+  // ======================= producer warp =================================
+  if (wid == C::NWC) {
+    if (lane != 0) return;
+    const uint64_t pol_u = P.upol ? policy_evict_normal() : policy_evict_last();  // u^n: halo re-reads
+    const uint64_t pol_s = policy_evict_first();   // u^{n-1}, vdt2: streamed once
+    // u plane p (local z, p >= zs-4) lives in u stage (p - zs + 4) % 9, use (p - zs + 4) / 9
+    auto issue_u = [&](int p, int st) {
+      mbar_arrive_expect_tx(&full_u[st], C::U_STAGE * 4);
+      tma_load_3d(su + st * C::U_STAGE, &tm_u, &full_u[st], bx0 - R, ty0 - R, p + R, pol_u);
+    };
+    // p plane p (p >= zs) lives in p stage (p - zs) % 3, use (p - zs) / 3
+    auto issue_p = [&](int p, int st) {
+      mbar_arrive_expect_tx(&full_p[st], 2 * C::P_STAGE * 4);
+      tma_load_3d(sup + st * C::P_STAGE, &tm_up, &full_p[st], cx0, ty0, p + R, pol_s);
+      tma_load_3d(sv + st * C::P_STAGE, &tm_v, &full_p[st], cx0, ty0, p, pol_s);
+    };
     for (int s = 0; s < SU; ++s)
       if (zs - R + s <= ze + R - 1) issue_u(zs - R + s, s);      // planes zs-4 .. zs+4
     for (int s = 0; s < SP; ++s)
       if (zs + s < ze) issue_p(zs + s, s);                       // planes zs .. zs+2
+    // refill in release order: when plane t is released, u plane t+9 and p plane t+3 go in
+#pragma unroll 1
+    for (int t = zs - R; t + SU <= ze + R - 1 || t + SP < ze; ++t) {
+      if (t + SU <= ze + R - 1) {
+        const int o = t - zs + R;
+        mbar_wait(&empty_u[o % SU], (o / SU) & 1);
+        issue_u(t + SU, o % SU);
+      }
+      if (t >= zs && t + SP < ze) {
+        const int o = t - zs;
+        mbar_wait(&empty_p[o % SP], (o / SP) & 1);
+        issue_p(t + SP, o % SP);
+      }
+      if (P.pf > 0) {
+        const int pu = t + SU + P.pf, pp = t + SP + P.pf;
+        if (pu <= ze + R - 1) tma_prefetch_3d(&tm_u, bx0 - R, ty0 - R, pu + R);
+        if (t >= zs && pp < ze) {
+          tma_prefetch_3d(&tm_up, cx0, ty0, pp + R);
+          tma_prefetch_3d(&tm_v, cx0, ty0, pp);
+        }
+      }
+    }
+    return;
   }
 
-  // ---- per-thread geometry: store mask, PML distances --------------------
+  // ======================= consumer warps ================================
+  const int lx = (wid % C::WX) * C::LXW + (lane % C::LXW);
+  const int ly = (wid / C::WX) * C::LYW + (lane / C::LXW);
+  const int gx = cx0 + 4 * lx;              // first x of my float4
+  const int gy = ty0 + ly * TYT;            // first y of my rows
+  // smem offsets (floats) of my float4 in row 0 of the tile, u stage / p stage
+  const int uo = (ly * TYT + R) * C::SW + cxo + 4 * lx + R;
+  const int po = (ly * TYT) * CW + 4 * lx;
+
+  // ---- per-thread geometry: store mask, PML coefficients -----------------
   unsigned mask = 0;                         // bit (r*4 + c): point is in the region
 #pragma unroll
   for (int r = 0; r < TYT; ++r)
@@ -228,6 +274,18 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
   PmlGeo PG;
   PG.nx = P.nx; PG.ny = P.ny; PG.nzg = P.nzg; PG.w = P.w; PG.T = TABN;
   PG.i2hx = P.k.i2h[0]; PG.i2hy = P.k.i2h[1]; PG.i2hz = P.k.i2h[2];
+  // fused mode: does any in-region point of my warp lie in the x/y PML?
+  bool warp_xy_pml = false;
+  if (MODE == MODE_FUSED) {
+    bool mine = false;
+#pragma unroll
+    for (int r = 0; r < TYT; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if ((mask >> (r * 4 + c)) & 1u)
+          mine |= dist1(gx + c, P.nx, P.w) > 0 || dist1(gy + r, P.ny, P.w) > 0;
+    warp_xy_pml = __any_sync(0xffffffffu, mine);
+  }
   // wall mode: z-invariant PML coefficients of my points, valid on planes with
   // dz(k-1) = dz(k) = dz(k+1) = 0:  cg_a = (eta(+e_a) - eta(-e_a)) / (2 h_a), A_d, B_d
   float cgx[TYT][4], cgy[TYT][4], A0[TYT][4], B0[TYT][4];
@@ -254,16 +312,14 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
   float4 q[9][TYT];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    mbar_wait(&bar_u[s], 0);
+    mbar_wait(&full_u[s], 0);
 #pragma unroll
     for (int r = 0; r < TYT; ++r) q[s][r] = lds4(su + s * C::U_STAGE + uo + r * C::SW);
   }
-  __syncthreads();                           // stages of planes zs-4..zs-1 are free
-  if (tid == 0) {
-    fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {                           // planes zs-4..zs-1 are not needed again
 #pragma unroll
-    for (int s = 0; s < R; ++s)
-      if (zs + 5 + s <= ze + R - 1) issue_u(zs + 5 + s, s);      // planes zs+5 .. zs+8
+    for (int s = 0; s < R; ++s) mbar_arrive(&empty_u[s]);
   }
 
   const Coef& K = P.k;
@@ -277,7 +333,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
       const int sl = (s + 8) % 9;            // slot/stage of the leading plane z+4
       const int sc = (s + 4) % 9;            // slot/stage of plane z
       // 1. leading plane z+4 -> queue
-      mbar_wait(&bar_u[sl], (j + (s >= 1 ? 1 : 0)) & 1);
+      mbar_wait(&full_u[sl], (j + (s >= 1 ? 1 : 0)) & 1);
 #pragma unroll
       for (int r = 0; r < TYT; ++r) q[sl][r] = lds4(su + sl * C::U_STAGE + uo + r * C::SW);
 
@@ -300,6 +356,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
       for (int r = 0; r < TYT; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c) L[r][c] = __fmul_rn(K.c0, f4get(Y[R + r], c));
+      if (MODE != MODE_NULL) {
 #pragma unroll
       for (int m = 1; m <= R; ++m)
 #pragma unroll
@@ -326,21 +383,33 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
             L[r][c] = __fmaf_rn(K.cz[m - 1],
                                 __fadd_rn(f4get(q[(s + 4 + m) % 9][r], c), f4get(q[(s + 4 - m + 9) % 9][r], c)),
                                 L[r][c]);
+      }
 
       // 3. u^{n-1}, vdt2 of plane z
       const int sp = s % 3;
-      mbar_wait(&bar_p[sp], (j + s / 3) & 1);
+      mbar_wait(&full_p[sp], (j + s / 3) & 1);
       float4 upv[TYT], vv[TYT];
 #pragma unroll
       for (int r = 0; r < TYT; ++r) {
-        upv[r] = lds4(sup + sp * C::P_STAGE + po + r * TX);
-        vv[r] = lds4(sv + sp * C::P_STAGE + po + r * TX);
+        upv[r] = lds4(sup + sp * C::P_STAGE + po + r * CW);
+        vv[r] = lds4(sv + sp * C::P_STAGE + po + r * CW);
+      }
+      // all smem reads of plane z done: release its stages to the producer
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty_u[sc]);
+        mbar_arrive(&empty_p[sp]);
       }
 
       // 4. update (one uniform branch per plane) and store
       const int kg = z + P.zoff;
       float4 res[TYT];
-      if (MODE == MODE_INNER) {
+      if (MODE == MODE_NULL) {
+#pragma unroll
+        for (int r = 0; r < TYT; ++r)
+          res[r] = make_float4(upv[r].x + vv[r].x + L[r][0], upv[r].y + vv[r].y, upv[r].z + vv[r].z,
+                               upv[r].w + vv[r].w);
+      } else if (MODE == MODE_INNER || (MODE == MODE_FUSED && !warp_xy_pml)) {
         if (kg >= P.w && kg < P.nzg - P.w) {
 #pragma unroll
           for (int r = 0; r < TYT; ++r) {
@@ -368,7 +437,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
                                 K.i2h[0], K.i2h[1], K.i2h[2]);
           }
         }
-      } else if (kg > P.w && kg < P.nzg - P.w - 1) {
+      } else if (MODE == MODE_WALL && kg > P.w && kg < P.nzg - P.w - 1) {
         // wall, z-interior plane: eta star is z-invariant (dz = 0 at k-1, k, k+1);
         // g = gx + gy (+ gz = +-0 exactly, dropped)
 #pragma unroll
@@ -388,7 +457,8 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
           res[r] = make_float4(o[0], o[1], o[2], o[3]);
         }
       } else {
-        // wall, plane in or next to a z cap: full 7-point eta star per point
+        // wall plane in / next to a z cap, or a fused-mode warp touching the x/y
+        // PML: full 7-point eta star per point (d = 0 points take the inner formula)
 #pragma unroll
         for (int r = 0; r < TYT; ++r) {
           const float4 Cu = Y[R + r];
@@ -410,22 +480,6 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
             if (mask & (1u << (r * 4 + c))) optr[r * P.pitch + c] = f4get(res[r], c);
       }
       optr += P.plane;
-
-      // 5. release the stages of plane z, refill them
-      __syncthreads();
-      if (tid == 0) {
-        fence_proxy_async_smem();
-        if (z + SU <= ze + R - 1) issue_u(z + SU, sc);
-        if (z + SP < ze) issue_p(z + SP, sp);
-        if (P.pf > 0) {
-          const int pu = z + SU + P.pf, pp = z + SP + P.pf;
-          if (pu <= ze + R - 1) tma_prefetch_3d(&tm_u, tx0 - R, ty0 - R, pu + R);
-          if (pp < ze) {
-            tma_prefetch_3d(&tm_up, tx0, ty0, pp + R);
-            tma_prefetch_3d(&tm_v, tx0, ty0, pp);
-          }
-        }
-      }
     }
   }
 }

@@ -56,34 +56,38 @@ static wave_status fail(wave_status st, const char* fmt, ...) {
 // ---------------------------------------------------------------------------
 struct KInfo {
   void* fn;
-  int tx, ty, nt;
+  int tx, cw, ty, nt;      // TMA box width, computed width, tile height, threads
   size_t (*smem)(int w);
   const char* name;
 };
 
-template <int TX, int TY, int TYT, int MODE>
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2>
 static KInfo kinfo(const char* name) {
-  return KInfo{(void*)k_stream<TX, TY, TYT, MODE>, TX, TY, StreamCfg<TX, TY, TYT>::NT,
-               &StreamCfg<TX, TY, TYT>::smem_bytes, name};
+  using C = StreamCfg<TX, CW, TY, TYT, MINB>;
+  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB>, TX, CW, TY, C::NT, &C::smem_bytes, name};
 }
 
 // interior-kernel variants (WAVE25_INNER_TILE selects one; default first)
 static const KInfo* inner_variants(int* n) {
   static const KInfo v[] = {
-      kinfo<128, 8, 1, MODE_INNER>("128x8x1"),
-      kinfo<64, 16, 1, MODE_INNER>("64x16x1"),
-      kinfo<128, 16, 1, MODE_INNER>("128x16x1"),
-      kinfo<64, 32, 2, MODE_INNER>("64x32x2"),
+      kinfo<128, 128, 8, 1, MODE_INNER>("128x8x1"),
+      kinfo<128, 128, 16, 1, MODE_INNER, 1>("128x16x1"),
+      kinfo<64, 64, 16, 1, MODE_INNER>("64x16x1"),
+      kinfo<128, 128, 8, 2, MODE_INNER, 1>("128x8x2"),
+      kinfo<128, 128, 8, 1, MODE_NULL>("null128x8x1"),      // memory-pattern probe (wrong results!)
+      kinfo<128, 128, 8, 1, MODE_FUSED>("fused128x8x1"),
+      kinfo<128, 128, 16, 1, MODE_NULL, 1>("null128x16x1"),
   };
   *n = (int)(sizeof v / sizeof v[0]);
   return v;
 }
 
+// x walls: 32-float (128-B) TMA boxes, 16 computed columns (w <= 16 per tile)
 static const KInfo* wallx_variants(int* n) {
   static const KInfo v[] = {
-      kinfo<32, 32, 1, MODE_WALL>("x32x32x1"),
-      kinfo<32, 64, 2, MODE_WALL>("x32x64x2"),
-      kinfo<32, 16, 1, MODE_WALL>("x32x16x1"),
+      kinfo<32, 16, 32, 1, MODE_WALL>("x32c16x32x1"),
+      kinfo<32, 16, 64, 1, MODE_WALL, 1>("x32c16x64x1"),
+      kinfo<32, 32, 32, 1, MODE_WALL>("x32c32x32x1"),
   };
   *n = (int)(sizeof v / sizeof v[0]);
   return v;
@@ -91,8 +95,8 @@ static const KInfo* wallx_variants(int* n) {
 
 static const KInfo* wally_variants(int* n) {
   static const KInfo v[] = {
-      kinfo<128, 16, 1, MODE_WALL>("y128x16x1"),
-      kinfo<64, 16, 1, MODE_WALL>("y64x16x1"),
+      kinfo<128, 128, 8, 1, MODE_WALL, 1>("y128x8x1"),
+      kinfo<128, 128, 16, 1, MODE_WALL, 1>("y128x16x1"),
   };
   *n = (int)(sizeof v / sizeof v[0]);
   return v;
@@ -106,7 +110,7 @@ static KInfo pick(const KInfo* v, int n, const char* env) {
   return v[0];
 }
 
-enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_N = 3 };
+enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_N = 4 };
 
 static KInfo g_k[KI_N];
 static void init_kernels() {
@@ -119,9 +123,11 @@ static void init_kernels() {
   g_k[KI_WALLX] = pick(v, n, "WAVE25_WALLX_TILE");
   v = wally_variants(&n);
   g_k[KI_WALLY] = pick(v, n, "WAVE25_WALLY_TILE");
+  g_k[KI_FUSED] = kinfo<128, 128, 8, 1, MODE_FUSED>("fused128x8x1");
   done = true;
 }
 #define KTX(ki) (g_k[ki].tx)
+#define KCW(ki) (g_k[ki].cw)
 #define KTY(ki) (g_k[ki].ty)
 
 static constexpr double W8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0};
@@ -163,8 +169,16 @@ struct wave_plan {
   Stats* stats_d = nullptr;
   // launch plans
   Maps maps[KI_N];
-  int occ[KI_N] = {1, 1, 1};
+  int occ[KI_N] = {1, 1, 1, 1};
+  bool fused = false;                // WAVE25_FUSED=1: one launch, per-warp paths (measured slower)
   int pf = 2;                        // L2 prefetch distance (WAVE25_PF), measured best
+  int prio_lo = 0, prio_hi = 0;      // stream priority range (launch attribute)
+  bool wall_prio = true;             // WAVE25_WALL_PRIO=0 disables
+  int order = 0;                     // tile order (WAVE25_ORDER)
+  int l2_persist_mb = 0;             // L2 set-aside for u (WAVE25_L2MB), 0 = off
+  float l2_hit_ratio = 1.f;          // WAVE25_L2HR
+  size_t max_window = 0;
+  int upol = 0;                      // u L2 policy (WAVE25_UPOL)
   std::vector<Launch> launches[3];   // [0] all planes, [1] edges, [2] interior
   // streams / graphs
   cudaStream_t side = nullptr, cap = nullptr;
@@ -274,14 +288,6 @@ static void* kernel_ptr(int ki) { return g_k[ki].fn; }
 static int kernel_threads(int ki) { return g_k[ki].nt; }
 static size_t kernel_smem(int ki, int w) { return g_k[ki].smem(w); }
 
-// x origin of a region's first tile: 4-aligned (float4 stores); a region
-// narrower than one tile (a thin x wall) gets a single tile ending at x1 so its
-// rows are whole TX-float segments (DRAM-friendly) instead of starting mid-row.
-static int tile_origin(int x0, int x1, int TX) {
-  if (x1 - x0 <= TX && x1 - TX >= 0) return std::min(x0, x1 - TX) & ~3;
-  return x0 & ~3;
-}
-
 // z-chunk length minimising (waves x (chunk + warm-up)) for ncol columns over nz planes
 static int choose_cz(int64_t ncol, int nz, int resident) {
   int best = nz;
@@ -316,6 +322,11 @@ static wave_status build_launches(wave_plan* P) {
   for (int s = 0; s < 3; ++s) {
     P->launches[s].clear();
     if (sets[s]->empty()) continue;
+    if (P->fused) {
+      // one launch over the whole plane, path per warp
+      add_regions(P, KI_FUSED, {{0, nx, 0, ny}}, *sets[s], &P->launches[s]);
+      continue;
+    }
     // interior kernel: inner xy footprint, all z (z caps plane-uniform)
     add_regions(P, KI_INNER, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
     // boundary kernels: left/right (x) walls; front/back (y) walls over full x
@@ -329,19 +340,21 @@ static wave_status build_launches(wave_plan* P) {
 
 static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 4>>& xy,
                         const std::vector<ZRange>& zr, std::vector<Launch>* out) {
-  const int TX = KTX(ki), TY = KTY(ki);
+  const int CW = KCW(ki), TY = KTY(ki);
   // chunk length from the largest z range and the total column count
   int64_t ncol = 0;
   int nzmax = 0;
   for (auto& b : xy) {
     if (b[1] <= b[0] || b[3] <= b[2]) continue;
-    const int ax0 = tile_origin(b[0], b[1], TX);
-    ncol += (int64_t)((b[1] - ax0 + TX - 1) / TX) * ((b[3] - b[2] + TY - 1) / TY);
+    const int ax0 = b[0] & ~3;
+    ncol += (int64_t)((b[1] - ax0 + CW - 1) / CW) * ((b[3] - b[2] + TY - 1) / TY);
   }
   for (auto& z : zr) nzmax = std::max(nzmax, z.z1 - z.z0);
   if (ncol == 0 || nzmax == 0) return;
   const int resident = P->occ[ki] * P->nsm;
-  const int cz = choose_cz(ncol * (int64_t)zr.size(), nzmax, resident);
+  int cz = choose_cz(ncol * (int64_t)zr.size(), nzmax, resident);
+  if (ki == KI_INNER)
+    if (const char* e = getenv("WAVE25_CZ")) cz = std::max(1, std::min(nzmax, atoi(e)));
 
   Launch Lc;
   Lc.ki = ki;
@@ -355,6 +368,8 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   p.tab = P->tab_d;
   p.cz = cz;
   p.pf = P->pf;
+  p.order = P->order;
+  p.upol = P->upol;
   int blk = 0;
   auto flush = [&]() {
     if (p.nreg == 0) return;
@@ -369,8 +384,8 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
       if (p.nreg == MAX_REGIONS) flush();
       Region& g = p.reg[p.nreg++];
       g.x0 = b[0]; g.x1 = b[1]; g.y0 = b[2]; g.y1 = b[3]; g.z0 = z.z0; g.z1 = z.z1;
-      g.ax0 = tile_origin(b[0], b[1], TX);
-      g.ntx = (b[1] - g.ax0 + TX - 1) / TX;
+      g.ax0 = b[0] & ~3;
+      g.ntx = (b[1] - g.ax0 + CW - 1) / CW;
       g.nty = (b[3] - b[2] + TY - 1) / TY;
       g.nzc = (z.z1 - z.z0 + cz - 1) / cz;
       g.blk0 = blk;
@@ -390,7 +405,31 @@ static wave_status launch_stream(wave_plan* P, const Launch& Lc, int cur, cudaSt
   const dim3 grid(Lc.nblk), block(kernel_threads(Lc.ki));
   const size_t smem = kernel_smem(Lc.ki, P->d.pml_width);
   void* args[] = {(void*)&M.u[cur], (void*)&M.up[1 - cur], (void*)&M.v, (void*)&p};
-  CK(cudaLaunchKernel(kernel_ptr(Lc.ki), grid, block, args, smem, s));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  // wall CTAs (compute-heavy) get priority so they interleave with the
+  // bandwidth-bound interior CTAs instead of trailing them
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = (Lc.ki != KI_INNER && Lc.ki != KI_FUSED && P->wall_prio) ? P->prio_hi : P->prio_lo;
+  int na = 1;
+  if (P->l2_persist_mb > 0) {
+    // L2 set-aside for u^n: its lines (re-read as neighbours' halos) persist,
+    // u_prev / vdt2 / u_next stream through the rest of L2
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = P->buf[cur];
+    attr[1].val.accessPolicyWindow.num_bytes = std::min<size_t>(P->L.elems_u * 4, P->max_window);
+    attr[1].val.accessPolicyWindow.hitRatio = P->l2_hit_ratio;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    na = 2;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  CK(cudaLaunchKernelExC(&cfg, kernel_ptr(Lc.ki), args));
   return WAVE_OK;
 }
 
@@ -435,7 +474,7 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, cudaStream_
   // fork: the interior kernel on s, the wall kernels on the side stream
   bool forked = false;
   for (size_t i = 0; i < Ls.size(); ++i) {
-    if (Ls[i].ki == KI_INNER || Ls.size() == 1) {
+    if (Ls[i].ki == KI_INNER || Ls[i].ki == KI_FUSED || Ls.size() == 1) {
       CKST(launch_stream(P, Ls[i], cur, s));
     } else {
       if (!forked) {
@@ -563,6 +602,23 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (get_encoder() != WAVE_OK) return bail(WAVE_ERR_CUDA);
   init_kernels();
   if (const char* e = getenv("WAVE25_PF")) P->pf = atoi(e);
+  if (const char* e = getenv("WAVE25_WALL_PRIO")) P->wall_prio = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
+  if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_UPOL")) P->upol = atoi(e);
+  cudaDeviceGetStreamPriorityRange(&P->prio_lo, &P->prio_hi);
+  if (const char* e = getenv("WAVE25_L2MB")) P->l2_persist_mb = atoi(e);
+  if (const char* e = getenv("WAVE25_L2HR")) P->l2_hit_ratio = (float)atof(e);
+  {
+    int mw = 0;
+    cudaDeviceGetAttribute(&mw, cudaDevAttrMaxAccessPolicyWindowSize, P->dev);
+    P->max_window = (size_t)mw;
+  }
+  if (P->l2_persist_mb > 0) {
+    int mx = 0;
+    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, P->dev);
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>((size_t)P->l2_persist_mb << 20, (size_t)mx));
+  }
   const int T = P->d.pml_width + 2;
   if ((e = cudaMalloc(&P->tab_d, 3 * T * sizeof(float))) != cudaSuccess ||
       (e = cudaMalloc(&P->dstep, sizeof(unsigned long long))) != cudaSuccess ||
@@ -622,12 +678,12 @@ wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
   const uint64_t pb = P->L.pitch_x * 4, plb = pb * P->d.ny;
   for (int ki = 0; ki < KI_N; ++ki) {
-    const uint32_t TX = KTX(ki), TY = KTY(ki);
+    const uint32_t TX = KTX(ki), CW = KCW(ki), TY = KTY(ki);
     for (int b = 0; b < 2; ++b) {
       CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
-      CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX, TY));
+      CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY));
     }
-    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, TX, TY));
+    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, CW, TY));
   }
   P->cur = 0;
   P->step = 0;
@@ -786,11 +842,12 @@ wave_status wave_step_finish(wave_plan* P) {
   return WAVE_OK;
 }
 
-wave_status wave_halo_views(const wave_plan* P, float** send_lo, float** send_hi, float** recv_lo,
-                            float** recv_hi, int64_t* count) {
+wave_status wave_halo_views(const wave_plan* P, int32_t which, float** send_lo, float** send_hi,
+                            float** recv_lo, float** recv_hi, int64_t* count) {
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
+  if (which != 0 && which != 1) return fail(WAVE_ERR_CONFIG, "which must be 0 or 1");
   const int64_t plane = P->L.pitch_x * P->d.ny, nz = P->d.nz;
-  float* b = P->buf[1 - P->cur];      // the buffer wave_step_edges writes
+  float* b = P->buf[which == 0 ? 1 - P->cur : P->cur];   // next (edges output) / current
   if (send_lo) *send_lo = b + R * plane;
   if (send_hi) *send_hi = b + nz * plane;
   if (recv_lo) *recv_lo = b;
@@ -834,13 +891,17 @@ int64_t wave_step_index(const wave_plan* P) { return P ? P->step : -1; }
 
 float wave_get_dt(const wave_plan* P) { return P ? P->dt : 0.f; }
 
+// measurement kind of a kernel (the fused launch is the interior kind: it is
+// the dominant kernel and covers every point)
+static int kk_of(int ki) { return ki == KI_FUSED ? WAVE_KK_INTERIOR : ki; }
+
 wave_status wave_kernel_points(const wave_plan* P, int64_t* out) {
   if (!P || !out) return fail(WAVE_ERR_CONFIG, "bad arguments");
   for (int k = 0; k < WAVE_KK_N; ++k) out[k] = 0;
   for (const Launch& L : P->launches[0])
     for (int r = 0; r < L.p.nreg; ++r) {
       const Region& g = L.p.reg[r];
-      out[L.ki] += (int64_t)(g.x1 - g.x0) * (g.y1 - g.y0) * (g.z1 - g.z0);
+      out[kk_of(L.ki)] += (int64_t)(g.x1 - g.x0) * (g.y1 - g.y0) * (g.z1 - g.z0);
     }
   out[WAVE_KK_SOURCE] = (P->src_set && P->src_local && P->ninc > 0) ? 1 : 0;
   return WAVE_OK;
@@ -868,7 +929,7 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
     bool forked = false;
     for (const Launch& L : P->launches[0]) {
       cudaStream_t ls = s;
-      if (L.ki != KI_INNER) {
+      if (L.ki != KI_INNER && L.ki != KI_FUSED) {
         if (!forked) {
           CK(cudaEventRecord(P->ev_fork, s));
           CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
@@ -876,7 +937,7 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
         }
         ls = P->side;
       }
-      CKST(mk(L.ki, ls));
+      CKST(mk(kk_of(L.ki), ls));
       CKST(launch_stream(P, L, cur, ls));
       CK(cudaEventRecord(recs.back().b, ls));
     }
@@ -913,8 +974,9 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
 int32_t wave_launches_per_step(const wave_plan* P) {
   if (!P) return -1;
   int n = 0;
-  if (P->d.kernel == WAVE_KERNEL_NAIVE) n = 1;
-  else n = (int)P->launches[0].size();
+  const bool split = P->d.nz != P->d.nz_global;     // slab plans step via edges + interior
+  if (P->d.kernel == WAVE_KERNEL_NAIVE) n = split ? 3 : 1;
+  else n = split ? (int)(P->launches[1].size() + P->launches[2].size()) : (int)P->launches[0].size();
   if (P->src_set && P->src_local && P->ninc > 0) n += 1;
   return n;
 }

@@ -94,6 +94,19 @@ class SlabRunner:
         self.stage_on_host = stage_on_host
         self.s_edge = torch.cuda.Stream(device=plan.device)
 
+    def exchange_current(self) -> None:
+        """Fill the ghost planes of the current u^n from the neighbours (needed
+        once when the run starts from a non-zero state)."""
+        if self.world == 1:
+            return
+        main = torch.cuda.current_stream(self.plan.device)
+        send_lo, send_hi, recv_lo, recv_hi = self.plan.halo_views(1)
+        works = halo_exchange(send_lo, send_hi, recv_lo, recv_hi, self.rank, self.world, self.group,
+                              self.stage_on_host)
+        for wk in works:
+            wk.wait()
+        main.synchronize()
+
     def step(self, n: int = 1) -> None:
         main = torch.cuda.current_stream(self.plan.device)
         for _ in range(n):

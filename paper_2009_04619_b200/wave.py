@@ -128,9 +128,10 @@ class WavePlan:
             _abi.wave_read(self._plan, which, out.data_ptr(), where, _stream_handle(stream))
         return out
 
-    def halo_views(self):
-        """(send_lo, send_hi, recv_lo, recv_hi) torch views of 4-plane blocks."""
-        a, b, c, d, n = _abi.wave_halo_views(self._plan)
+    def halo_views(self, which: int = 0):
+        """(send_lo, send_hi, recv_lo, recv_hi) torch views of 4-plane blocks;
+        which = 0: in the buffer the edges step writes, 1: in the current u^n."""
+        a, b, c, d, n = _abi.wave_halo_views(self._plan, which)
         out = []
         for p in (a, b, c, d):
             for buf in self.bufs:

@@ -195,11 +195,11 @@ def test_slabs_on_one_gpu_bitwise(nslab):
         for p, _, _ in plans:
             p.step_edges()
         for r, (p, off, nzl) in enumerate(plans):
-            send_lo, send_hi, recv_lo, recv_hi = p.halo_views()
+            send_lo, send_hi, recv_lo, recv_hi = p.halo_views(0)
             if r > 0:
-                plans[r - 1][0].halo_views()[3].copy_(send_lo)
+                plans[r - 1][0].halo_views(0)[3].copy_(send_lo)
             if r < nslab - 1:
-                plans[r + 1][0].halo_views()[2].copy_(send_hi)
+                plans[r + 1][0].halo_views(0)[2].copy_(send_hi)
         for p, _, _ in plans:
             p.step_interior()
             p.step_finish()
@@ -294,3 +294,58 @@ def test_full_size_sampled_slabs(sname):
     zt = [(0, 6), (n // 2 - 3, n // 2 + 3), (n - 6, n)]
     err = _full_size_slab_check(sname, 5, zt)
     assert err <= TOL, err
+
+
+def _slab_worker(rank, world, port, steps, q):
+    import os
+    import torch.distributed as dist
+    from paper_2009_04619_b200.dist import SlabRunner, slab_bounds
+    from paper_2009_04619_b200.wave import WavePlan as WP
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        s = synth.scenario("RAGGED")
+        sh = (s.nz, s.ny, s.nx)
+        u0, um1 = synth.random_state(sh, 31), synth.random_state(sh, 32)
+        off, nzl = slab_bounds(s.nz, rank, world)
+        p = WP(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
+        p.set_velocity(synth.velocity(s)[off:off + nzl])
+        p.set_source(*s.source, synth.wavelet_for(s, steps))
+        p.set_state(um1[off:off + nzl], u0[off:off + nzl])
+        runner = SlabRunner(p, rank, world, stage_on_host=True)
+        runner.exchange_current()
+        runner.step(steps)
+        torch.cuda.synchronize()
+        q.put((rank, p.read(0).cpu().numpy()))
+        p.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_runner_two_processes_bitwise():
+    # the multi-process driver (SlabRunner: edges -> halo exchange || interior)
+    # with 2 ranks on one GPU over gloo == the single-plan run, bitwise
+    import socket
+    import torch.multiprocessing as mp
+    steps = 17
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, steps, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    parts = sorted(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    got = np.concatenate([a for _, a in parts], axis=0)
+    s = synth.scenario("RAGGED")
+    sh = (s.nz, s.ny, s.nx)
+    ref, _ = run_gpu(s, steps, synth.random_state(sh, 31), synth.random_state(sh, 32),
+                     wl=synth.wavelet_for(s, steps))
+    assert np.array_equal(got, ref)
