@@ -471,21 +471,19 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, cudaStream_
   }
   const std::vector<Launch>& Ls = P->launches[which];
   if (Ls.empty()) return WAVE_OK;
-  // fork: the interior kernel on s, the wall kernels on the side stream
-  bool forked = false;
-  for (size_t i = 0; i < Ls.size(); ++i) {
-    if (Ls[i].ki == KI_INNER || Ls[i].ki == KI_FUSED || Ls.size() == 1) {
-      CKST(launch_stream(P, Ls[i], cur, s));
-    } else {
-      if (!forked) {
-        CK(cudaEventRecord(P->ev_fork, s));
-        CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
-        forked = true;
-      }
-      CKST(launch_stream(P, Ls[i], cur, P->side));
-    }
+  // fork BEFORE any launch: the wall kernels (side stream, high priority) and
+  // the interior kernel (stream s) run concurrently; join before the source
+  bool walls = false;
+  for (const Launch& L : Ls) walls |= (L.ki == KI_WALLX || L.ki == KI_WALLY);
+  if (walls) {
+    CK(cudaEventRecord(P->ev_fork, s));
+    CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
+    for (const Launch& L : Ls)
+      if (L.ki == KI_WALLX || L.ki == KI_WALLY) CKST(launch_stream(P, L, cur, P->side));
   }
-  if (forked) {
+  for (const Launch& L : Ls)
+    if (L.ki != KI_WALLX && L.ki != KI_WALLY) CKST(launch_stream(P, L, cur, s));
+  if (walls) {
     CK(cudaEventRecord(P->ev_join, P->side));
     CK(cudaStreamWaitEvent(s, P->ev_join, 0));
   }
@@ -926,22 +924,22 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
   wave_status st = WAVE_OK;
   for (int64_t n = 0; n < nsteps && st == WAVE_OK; ++n) {
     const int cur = P->cur;
-    bool forked = false;
-    for (const Launch& L : P->launches[0]) {
-      cudaStream_t ls = s;
-      if (L.ki != KI_INNER && L.ki != KI_FUSED) {
-        if (!forked) {
-          CK(cudaEventRecord(P->ev_fork, s));
-          CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
-          forked = true;
-        }
-        ls = P->side;
-      }
-      CKST(mk(kk_of(L.ki), ls));
-      CKST(launch_stream(P, L, cur, ls));
-      CK(cudaEventRecord(recs.back().b, ls));
+    bool walls = false;
+    for (const Launch& L : P->launches[0]) walls |= (L.ki == KI_WALLX || L.ki == KI_WALLY);
+    if (walls) {
+      CK(cudaEventRecord(P->ev_fork, s));
+      CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     }
-    if (forked) {
+    for (int pass = 0; pass < 2; ++pass)          // walls (side stream) first, then interior
+      for (const Launch& L : P->launches[0]) {
+        const bool is_wall = L.ki == KI_WALLX || L.ki == KI_WALLY;
+        if (is_wall != (pass == 0)) continue;
+        cudaStream_t ls = is_wall ? P->side : s;
+        CKST(mk(kk_of(L.ki), ls));
+        CKST(launch_stream(P, L, cur, ls));
+        CK(cudaEventRecord(recs.back().b, ls));
+      }
+    if (walls) {
       CK(cudaEventRecord(P->ev_join, P->side));
       CK(cudaStreamWaitEvent(s, P->ev_join, 0));
     }
