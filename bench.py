@@ -342,7 +342,8 @@ def run_ours(args, rank, world, local):
                 "kernel_ms_per_step": {k: v / max(args.steps, 1) for k, v in kms.items()},
                 "kernel_points_per_step": kpts,
                 "share_of_step": kms["interior"] / max(sum(kms.values()), 1e-9),
-                "how": "CUDA events around each launch on its stream, profiled pass of K steps (direct launches)"}
+                "how": "CUDA events around each launch on the launching stream, profiled pass of K steps "
+                       "(direct launches serialized on that stream, so each event pair times one kernel)"}
         if not args.no_probe:
             roof["practical_roof_gbs_3r1w"] = roof_probe(torch)
             roof["frac_of_practical_roof"] = achieved / roof["practical_roof_gbs_3r1w"]

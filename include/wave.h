@@ -260,9 +260,10 @@ enum { WAVE_KK_INTERIOR = 0, WAVE_KK_XWALLS = 1, WAVE_KK_YWALLS = 2, WAVE_KK_SOU
  * (16 B per point-step).  out[WAVE_KK_N]. */
 WAVE_API wave_status wave_kernel_points(const wave_plan *plan, int64_t *out);
 
-/* Like wave_step (same kernels, same streams, direct launches instead of the
- * CUDA graph) but with a CUDA event pair around every kernel launch, each on
- * the stream that launches it.  Synchronises `stream` at the end and returns
+/* Like wave_step (same kernels and launch configurations, direct launches
+ * instead of the CUDA graph) but serialized on `stream` with a CUDA event pair
+ * around every kernel launch, so each pair times one kernel alone.
+ * Synchronises `stream` at the end and returns
  * the summed device time of each kernel kind over the nsteps in
  * kernel_ms[WAVE_KK_N] and the number of launches of each kind in
  * launches[WAVE_KK_N] (either may be NULL).  Single-slab plans only. */

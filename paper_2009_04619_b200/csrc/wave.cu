@@ -95,8 +95,8 @@ static const KInfo* wallx_variants(int* n) {
 
 static const KInfo* wally_variants(int* n) {
   static const KInfo v[] = {
-      kinfo<128, 128, 8, 1, MODE_WALL, 1>("y128x8x1"),
       kinfo<128, 128, 16, 1, MODE_WALL, 1>("y128x16x1"),
+      kinfo<128, 128, 8, 1, MODE_WALL, 1>("y128x8x1"),
   };
   *n = (int)(sizeof v / sizeof v[0]);
   return v;
@@ -171,7 +171,7 @@ struct wave_plan {
   Maps maps[KI_N];
   int occ[KI_N] = {1, 1, 1, 1};
   bool fused = false;                // WAVE25_FUSED=1: one launch, per-warp paths (measured slower)
-  int pf = 2;                        // L2 prefetch distance (WAVE25_PF), measured best
+  int pf = 1;                        // L2 prefetch distance (WAVE25_PF), measured best
   int prio_lo = 0, prio_hi = 0;      // stream priority range (launch attribute)
   bool wall_prio = true;             // WAVE25_WALL_PRIO=0 disables
   int order = 0;                     // tile order (WAVE25_ORDER)
@@ -924,24 +924,11 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
   wave_status st = WAVE_OK;
   for (int64_t n = 0; n < nsteps && st == WAVE_OK; ++n) {
     const int cur = P->cur;
-    bool walls = false;
-    for (const Launch& L : P->launches[0]) walls |= (L.ki == KI_WALLX || L.ki == KI_WALLY);
-    if (walls) {
-      CK(cudaEventRecord(P->ev_fork, s));
-      CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
-    }
-    for (int pass = 0; pass < 2; ++pass)          // walls (side stream) first, then interior
-      for (const Launch& L : P->launches[0]) {
-        const bool is_wall = L.ki == KI_WALLX || L.ki == KI_WALLY;
-        if (is_wall != (pass == 0)) continue;
-        cudaStream_t ls = is_wall ? P->side : s;
-        CKST(mk(kk_of(L.ki), ls));
-        CKST(launch_stream(P, L, cur, ls));
-        CK(cudaEventRecord(recs.back().b, ls));
-      }
-    if (walls) {
-      CK(cudaEventRecord(P->ev_join, P->side));
-      CK(cudaStreamWaitEvent(s, P->ev_join, 0));
+    // serialized on `stream` so every event pair brackets one kernel alone
+    for (const Launch& L : P->launches[0]) {
+      CKST(mk(kk_of(L.ki), s));
+      CKST(launch_stream(P, L, cur, s));
+      CK(cudaEventRecord(recs.back().b, s));
     }
     if (P->src_set && P->src_local && P->ninc > 0) {
       CKST(mk(WAVE_KK_SOURCE, s));
