@@ -54,11 +54,14 @@ __device__ __forceinline__ float gterm(float ep, float em, float u1p, float u1m,
 }
 
 // PML update: ((2u - A u_prev) + vdt2 (L + g)) / B with a true
-// IEEE division (a reciprocal multiply drifts past the 1e-5 gate, R9)
+// IEEE division (a reciprocal multiply drifts past the 1e-5 gate, R9).
+// 0 / B (B >= 1) is +-0 exactly; testing for it keeps quiet PML cells (u = 0
+// before the wave arrives) off the software slow path of __fdiv_rn.
 __device__ __forceinline__ float upd_pml(float L, float g, float c, float up, float v,
                                          float A, float B) {
   const float t = __fmaf_rn(-A, up, __fmul_rn(2.0f, c));
-  return __fdiv_rn(__fmaf_rn(v, __fadd_rn(L, g), t), B);
+  const float num = __fmaf_rn(v, __fadd_rn(L, g), t);
+  return num == 0.0f ? num : __fdiv_rn(num, B);
 }
 
 // Distance (cells) to the inner box along one axis: 0 inside [w, n-w), 1..w

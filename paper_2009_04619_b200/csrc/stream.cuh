@@ -286,24 +286,43 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
           mine |= dist1(gx + c, P.nx, P.w) > 0 || dist1(gy + r, P.ny, P.w) > 0;
     warp_xy_pml = __any_sync(0xffffffffu, mine);
   }
-  // wall mode: z-invariant PML coefficients of my points, valid on planes with
-  // dz(k-1) = dz(k) = dz(k+1) = 0:  cg_a = (eta(+e_a) - eta(-e_a)) / (2 h_a), A_d, B_d
-  float cgx[TYT][4], cgy[TYT][4], A0[TYT][4], B0[TYT][4];
+  // wall mode, planes with dz(k-1) = dz(k) = dz(k+1) = 0: a warp whose points
+  // all have dx = 0 (y wall away from the corners) has a row-uniform eta star
+  // (grad eta = d_y eta only); one whose points all have dy = 0 (x wall) a
+  // column-constant one (d_x eta only).  Precompute those coefficients once:
+  //   cg = (eta(+e_a) - eta(-e_a)) / (2 h_a), A_d, B_d
+  // Warps mixing both (corners) take the general path.
+  int wkind = 0;                             // 1: y-wall rows, 2: x-wall columns, 0: general
+  float cgr[TYT], Ar[TYT], Br[TYT];          // y-wall: per row
+  float cgc[4], Ac[4], Bc[4];                // x-wall: per column
   if (MODE == MODE_WALL) {
+    bool all_dx0 = true, all_dy0 = true;
+#pragma unroll
+    for (int r = 0; r < TYT; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if ((mask >> (r * 4 + c)) & 1u) {
+          all_dx0 &= dist1(gx + c, P.nx, P.w) == 0;
+          all_dy0 &= dist1(gy + r, P.ny, P.w) == 0;
+        }
+    all_dx0 = __all_sync(0xffffffffu, all_dx0);
+    all_dy0 = __all_sync(0xffffffffu, all_dy0);
+    wkind = all_dx0 ? 1 : (all_dy0 ? 2 : 0);
 #pragma unroll
     for (int r = 0; r < TYT; ++r) {
       const int dy = dist1(gy + r, P.ny, P.w);
-      const int dyp = dist1(gy + r + 1, P.ny, P.w), dym = dist1(gy + r - 1, P.ny, P.w);
+      cgr[r] = __fmul_rn(__fsub_rn(stab[dist1(gy + r + 1, P.ny, P.w)], stab[dist1(gy + r - 1, P.ny, P.w)]),
+                         PG.i2hy);
+      Ar[r] = stab[TABN + dy];
+      Br[r] = stab[2 * TABN + dy];
+    }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int dx = dist1(gx + c, P.nx, P.w);
-        const int d0 = max(dx, dy);
-        cgx[r][c] = __fmul_rn(__fsub_rn(stab[max(dist1(gx + c + 1, P.nx, P.w), dy)],
-                                        stab[max(dist1(gx + c - 1, P.nx, P.w), dy)]), PG.i2hx);
-        cgy[r][c] = __fmul_rn(__fsub_rn(stab[max(dx, dyp)], stab[max(dx, dym)]), PG.i2hy);
-        A0[r][c] = stab[TABN + d0];
-        B0[r][c] = stab[2 * TABN + d0];
-      }
+    for (int c = 0; c < 4; ++c) {
+      const int dx = dist1(gx + c, P.nx, P.w);
+      cgc[c] = __fmul_rn(__fsub_rn(stab[dist1(gx + c + 1, P.nx, P.w)], stab[dist1(gx + c - 1, P.nx, P.w)]),
+                         PG.i2hx);
+      Ac[c] = stab[TABN + dx];
+      Bc[c] = stab[2 * TABN + dx];
     }
   }
   float* optr = P.out + (int64_t)(zs + R) * P.plane + (int64_t)gy * P.pitch + gx;
@@ -437,22 +456,28 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
                                 K.i2h[0], K.i2h[1], K.i2h[2]);
           }
         }
-      } else if (MODE == MODE_WALL && kg > P.w && kg < P.nzg - P.w - 1) {
-        // wall, z-interior plane: eta star is z-invariant (dz = 0 at k-1, k, k+1);
-        // g = gx + gy (+ gz = +-0 exactly, dropped)
+      } else if (MODE == MODE_WALL && wkind != 0 && kg > P.w && kg < P.nzg - P.w - 1) {
+        // wall, z-interior plane, pure y-wall rows (g = gy) or pure x-wall
+        // columns (g = gx); the other two grad terms are +-0 exactly (dropped)
 #pragma unroll
         for (int r = 0; r < TYT; ++r) {
           const float4 Cu = Y[R + r];
           const float X[12] = {Lf[r].x, Lf[r].y, Lf[r].z, Lf[r].w, Cu.x, Cu.y,
                                Cu.z, Cu.w, Rf[r].x, Rf[r].y, Rf[r].z, Rf[r].w};
           float o[4];
+          if (wkind == 1) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float gxa = __fmul_rn(cgx[r][c], __fmul_rn(__fsub_rn(X[5 + c], X[3 + c]), K.i2h[0]));
-            const float gya = __fmul_rn(cgy[r][c], __fmul_rn(__fsub_rn(f4get(Y[R + r + 1], c),
-                                                                       f4get(Y[R + r - 1], c)), K.i2h[1]));
-            o[c] = upd_pml(L[r][c], __fadd_rn(gxa, gya), X[4 + c], f4get(upv[r], c), f4get(vv[r], c),
-                           A0[r][c], B0[r][c]);
+            for (int c = 0; c < 4; ++c) {
+              const float gya = __fmul_rn(cgr[r], __fmul_rn(__fsub_rn(f4get(Y[R + r + 1], c),
+                                                                      f4get(Y[R + r - 1], c)), K.i2h[1]));
+              o[c] = upd_pml(L[r][c], gya, X[4 + c], f4get(upv[r], c), f4get(vv[r], c), Ar[r], Br[r]);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float gxa = __fmul_rn(cgc[c], __fmul_rn(__fsub_rn(X[5 + c], X[3 + c]), K.i2h[0]));
+              o[c] = upd_pml(L[r][c], gxa, X[4 + c], f4get(upv[r], c), f4get(vv[r], c), Ac[c], Bc[c]);
+            }
           }
           res[r] = make_float4(o[0], o[1], o[2], o[3]);
         }

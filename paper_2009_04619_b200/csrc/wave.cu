@@ -95,8 +95,8 @@ static const KInfo* wallx_variants(int* n) {
 
 static const KInfo* wally_variants(int* n) {
   static const KInfo v[] = {
-      kinfo<128, 128, 16, 1, MODE_WALL, 1>("y128x16x1"),
       kinfo<128, 128, 8, 1, MODE_WALL, 1>("y128x8x1"),
+      kinfo<128, 128, 16, 1, MODE_WALL, 1>("y128x16x1"),
   };
   *n = (int)(sizeof v / sizeof v[0]);
   return v;
