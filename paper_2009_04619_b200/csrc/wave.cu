@@ -82,10 +82,12 @@ static const KInfo* inner_variants(int* n) {
   return v;
 }
 
-// x walls: 32-float (128-B) TMA boxes, 16 computed columns (w <= 16 per tile)
+// x walls: 16 computed columns per tile; 24 + 8 = 32-float (128-B) u boxes
 static const KInfo* wallx_variants(int* n) {
   static const KInfo v[] = {
+      kinfo<24, 16, 32, 1, MODE_WALL>("x24c16x32x1"),
       kinfo<32, 16, 32, 1, MODE_WALL>("x32c16x32x1"),
+      kinfo<24, 16, 64, 1, MODE_WALL, 1>("x24c16x64x1"),
       kinfo<32, 16, 64, 1, MODE_WALL, 1>("x32c16x64x1"),
       kinfo<32, 32, 32, 1, MODE_WALL>("x32c32x32x1"),
   };
