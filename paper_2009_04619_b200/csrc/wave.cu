@@ -86,6 +86,8 @@ static const KInfo* inner_variants(int* n) {
 static const KInfo* wallx_variants(int* n) {
   static const KInfo v[] = {
       kinfo<24, 16, 32, 1, MODE_WALL>("x24c16x32x1"),
+      kinfo<24, 16, 32, 1, MODE_WALL, 3>("x24c16x32x1m3"),
+      kinfo<24, 16, 32, 1, MODE_WALL, 4>("x24c16x32x1m4"),
       kinfo<32, 16, 32, 1, MODE_WALL>("x32c16x32x1"),
       kinfo<24, 16, 64, 1, MODE_WALL, 1>("x24c16x64x1"),
       kinfo<32, 16, 64, 1, MODE_WALL, 1>("x32c16x64x1"),
@@ -97,7 +99,9 @@ static const KInfo* wallx_variants(int* n) {
 
 static const KInfo* wally_variants(int* n) {
   static const KInfo v[] = {
+      kinfo<64, 64, 8, 1, MODE_WALL, 3>("y64x8x1m3"),
       kinfo<128, 128, 8, 1, MODE_WALL, 1>("y128x8x1"),
+      kinfo<128, 128, 8, 1, MODE_WALL, 2>("y128x8x1m2"),
       kinfo<128, 128, 16, 1, MODE_WALL, 1>("y128x16x1"),
   };
   *n = (int)(sizeof v / sizeof v[0]);

@@ -349,3 +349,42 @@ def test_slab_runner_two_processes_bitwise():
     ref, _ = run_gpu(s, steps, synth.random_state(sh, 31), synth.random_state(sh, 32),
                      wl=synth.wavelet_for(s, steps))
     assert np.array_equal(got, ref)
+
+
+VARIANT_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, synth
+from paper_2009_04619_b200.wave import WavePlan
+for name in ("RAGGED", "C1"):
+    s = synth.scenario(name)
+    sh = (s.nz, s.ny, s.nx)
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    p.set_velocity(synth.velocity(s))
+    p.set_source(*s.source, synth.wavelet_for(s, 12))
+    p.set_state(synth.random_state(sh, 41), synth.random_state(sh, 42))
+    p.step(12)
+    print(name, hashlib.sha256(p.read(0).cpu().numpy().tobytes()).hexdigest())
+    p.close()
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"WAVE25_INNER_TILE": "128x16x1"}, {"WAVE25_INNER_TILE": "64x16x1"},
+    {"WAVE25_WALLX_TILE": "x32c16x32x1"}, {"WAVE25_WALLX_TILE": "x24c16x64x1"},
+    {"WAVE25_WALLY_TILE": "y128x8x1"}, {"WAVE25_WALLY_TILE": "y128x16x1"},
+    {"WAVE25_FUSED": "1"}, {"WAVE25_FORK": "0", "WAVE25_PF": "0"}, {"WAVE25_CZ": "7"},
+])
+def test_kernel_variants_bitwise(env):
+    # every tile / scheduling variant used in the DESIGN.md ablations computes
+    # the same values as the default configuration, bitwise
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("WAVE25_")}
+    ref = subprocess.run([sys.executable, "-c", VARIANT_SCRIPT, root], env=base, capture_output=True,
+                         text=True, check=True).stdout
+    got = subprocess.run([sys.executable, "-c", VARIANT_SCRIPT, root], env={**base, **env},
+                         capture_output=True, text=True, check=True).stdout
+    assert ref.count("\n") == 2 and got == ref
