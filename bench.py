@@ -253,7 +253,7 @@ def run_ours(args, rank, world, local):
     import synth
     import __graft_entry__
     from paper_2009_04619_b200.wave import WavePlan
-    from paper_2009_04619_b200.dist import SlabRunner, slab_bounds
+    from paper_2009_04619_b200.dist import PeerSlabRunner, SlabRunner, slab_bounds
 
     __graft_entry__.build_cuda()
     local = local % max(torch.cuda.device_count(), 1)
@@ -291,8 +291,14 @@ def run_ours(args, rank, world, local):
     plan = WavePlan(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
     plan.set_velocity(V)
     plan.set_source(*s.source, wl)
-    runner = (SlabRunner(plan, rank, world, stage_on_host=os.environ.get("WAVE25_DIST_BACKEND", "nccl") != "nccl")
-              if world > 1 else None)
+    halo = os.environ.get("WAVE25_HALO", "peer")     # peer: fused peer stores; nccl: send/recv
+    if world == 1:
+        runner = None
+    elif halo == "peer":
+        runner = PeerSlabRunner(plan, rank, world)
+    else:
+        runner = SlabRunner(plan, rank, world,
+                            stage_on_host=os.environ.get("WAVE25_DIST_BACKEND", "nccl") != "nccl")
     stream = torch.cuda.current_stream()
 
     def steps(n):
@@ -385,7 +391,10 @@ def run_ours(args, rank, world, local):
                        "pml_width": s.w, "parallelism": f"z-slab x{world}" if world > 1 else "1 GPU",
                        "l2": f"no flush: {BYTES_PER_POINT * pts_total / 1e9:.1f} GB streamed per step >> 126 MB L2",
                        "kernels": "interior + x-walls + y-walls (2 streams, joined) + source, CUDA graph"
-                                  if world == 1 else "edges -> NCCL halo send/recv || interior, joined"},
+                                  if world == 1 else (
+                                      "fused halo: stencil kernels store edge planes into the neighbours' ghost "
+                                      "planes over NVLink (IPC peer mapping) + device step flags, CUDA graph"
+                                      if halo == "peer" else "edges -> NCCL send/recv || interior, joined")},
             "hbm_gbs_at_16B": value * BYTES_PER_POINT,
             "frac_of_measured_hbm": value * BYTES_PER_POINT / measured_peak()[0],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

@@ -221,6 +221,44 @@ WAVE_API wave_status wave_halo_views(const wave_plan *plan, int32_t which, float
                                      float **send_hi, float **recv_lo, float **recv_hi,
                                      int64_t *count);
 
+/* ---- fused peer-store halo exchange (z-slab runs, one GPU per rank) ------ */
+
+/* Neighbour wiring for wave_step_peer.  All pointers are device pointers valid
+ * in this process (peer / IPC mappings of the neighbours' buffers, e.g. opened
+ * with cudaIpcOpenMemHandle over NVLink); NULL where there is no neighbour.
+ * Every rank must bind its buffers in the same order and step in lockstep so
+ * that buffer parity agrees.  Ownership stays with the caller. */
+typedef struct {
+    float *lo_buf[2];        /* lower (z_offset-1) neighbour's wavefield buffers 0/1 */
+    float *hi_buf[2];        /* upper neighbour's wavefield buffers 0/1             */
+    int64_t lo_nz;           /* lower neighbour's nz (locates its upper ghosts)    */
+    uint64_t *my_flags;      /* this rank's 2 flag words (device, zero-initialised):
+                                [0] steps completed by the lower neighbour,
+                                [1] steps completed by the upper neighbour        */
+    uint64_t *lo_flags;      /* lower neighbour's flag words (peer pointer)       */
+    uint64_t *hi_flags;      /* upper neighbour's flag words (peer pointer)       */
+} wave_peers;
+
+/* Install (or clear, with NULL) the neighbour wiring.  Resets the step
+ * counters used by the flag protocol. */
+WAVE_API wave_status wave_set_peers(wave_plan *plan, const wave_peers *peers);
+
+/* Advance nsteps steps on a z-slab with the halo exchange fused into the
+ * compute: every step (a) waits until both neighbours have completed the
+ * previous step (acquire loads of my_flags), (b) runs the interior and wall
+ * kernels over all local planes; CTAs that compute planes [0,4) / [nz-4,nz)
+ * also store them straight into the lower / upper neighbour's ghost planes of
+ * the next buffer, (c) adds the source (mirrored into the neighbour's ghost if
+ * on an edge plane), (d) publishes its completed-step count to both
+ * neighbours (system-scope fence + release stores).  No NCCL in the step;
+ * replayed from CUDA graphs. */
+WAVE_API wave_status wave_step_peer(wave_plan *plan, int64_t nsteps, void *stream);
+
+/* Copy this slab's 4 edge planes of u^n (which = 1) or of the next buffer
+ * (which = 0) into the neighbours' ghost planes (for a non-zero initial
+ * state); enqueued on `stream`, no flag traffic. */
+WAVE_API wave_status wave_push_halo(wave_plan *plan, int32_t which, void *stream);
+
 /* ---- outputs ------------------------------------------------------------- */
 
 /* Copy u^n (which = 0) or u^{n-1} (which = 1) to dst, dense [nz][ny][nx] fp32

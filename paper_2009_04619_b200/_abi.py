@@ -27,7 +27,7 @@ EXPORTS = [
     "wave_set_source", "wave_set_state", "wave_step", "wave_step_edges", "wave_step_interior",
     "wave_step_finish", "wave_halo_views", "wave_read", "wave_field_ptr", "wave_check_finite",
     "wave_step_index", "wave_get_dt", "wave_launches_per_step", "wave_kernel_points",
-    "wave_step_profiled",
+    "wave_step_profiled", "wave_set_peers", "wave_step_peer", "wave_push_halo",
 ]
 KERNEL_KINDS = ["interior", "xwalls", "ywalls", "source"]
 
@@ -49,6 +49,11 @@ class WaveLayout(ctypes.Structure):
 class WaveRegion(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("reserved0", ctypes.c_int32),
                 ("lo", ctypes.c_int64 * 3), ("ext", ctypes.c_int64 * 3)]
+
+
+class WavePeers(ctypes.Structure):
+    _fields_ = [("lo_buf", ctypes.c_void_p * 2), ("hi_buf", ctypes.c_void_p * 2), ("lo_nz", ctypes.c_int64),
+                ("my_flags", ctypes.c_void_p), ("lo_flags", ctypes.c_void_p), ("hi_flags", ctypes.c_void_p)]
 
 
 class WaveError(RuntimeError):
@@ -100,6 +105,9 @@ def lib() -> ctypes.CDLL:
                 "wave_launches_per_step": ([P], i32),
                 "wave_kernel_points": ([P, P], i32),
                 "wave_step_profiled": ([P, i64, P, P, P], i32),
+                "wave_set_peers": ([P, ctypes.POINTER(WavePeers)], i32),
+                "wave_step_peer": ([P, i64, P], i32),
+                "wave_push_halo": ([P, i32, P], i32),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)
@@ -244,3 +252,16 @@ def wave_step_profiled(plan, nsteps: int, stream: int):
     n = np.zeros(4, np.int64)
     check(lib().wave_step_profiled(plan, int(nsteps), stream, ms.ctypes.data, n.ctypes.data))
     return dict(zip(KERNEL_KINDS, (float(v) for v in ms))), dict(zip(KERNEL_KINDS, (int(v) for v in n)))
+
+
+def wave_set_peers(plan, peers) -> None:
+    """peers: WavePeers or None (clears)."""
+    check(lib().wave_set_peers(plan, ctypes.byref(peers) if peers is not None else None))
+
+
+def wave_step_peer(plan, nsteps: int, stream: int) -> None:
+    check(lib().wave_step_peer(plan, int(nsteps), stream))
+
+
+def wave_push_halo(plan, which: int, stream: int) -> None:
+    check(lib().wave_push_halo(plan, int(which), stream))

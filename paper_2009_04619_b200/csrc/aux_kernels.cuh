@@ -65,11 +65,63 @@ __global__ void __launch_bounds__(128) k_naive(const float* __restrict__ u, floa
 
 // Source injection, PAPER.md L263 (Alg. 1) / SPEC.md L158-161: u_next[src] +=
 // inc[n], n = the device step counter (so replayed CUDA graphs stay correct).
+// `mirror` (or null): the same cell in a neighbour's ghost planes (fused halo
+// exchange), which must carry the injected value too.
 __global__ void k_source(float* __restrict__ buf, int64_t off, const float* __restrict__ inc,
-                         int64_t ninc, unsigned long long* __restrict__ dstep) {
+                         int64_t ninc, unsigned long long* __restrict__ dstep, float* mirror) {
   const unsigned long long n = *dstep;
-  if (n < (unsigned long long)ninc) buf[off] = __fadd_rn(buf[off], inc[n]);
+  if (n < (unsigned long long)ninc) {
+    const float v = __fadd_rn(buf[off], inc[n]);
+    buf[off] = v;
+    if (mirror) *mirror = v;
+  }
   *dstep = n + 1;
+}
+
+// ---- fused halo exchange: neighbour step flags (system scope) -------------
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Wait until the neighbours have completed as many steps as this rank.  The
+// spin is bounded (~10 s): a mis-wired or dead neighbour traps (a CUDA error
+// on this rank) instead of hanging the GPU.
+__global__ void k_peer_wait(const unsigned long long* flags, const unsigned long long* done, int need_lo,
+                            int need_hi) {
+  const unsigned long long d = *done;
+  unsigned long long spins = 0;
+  if (need_lo)
+    while (ld_acquire_sys(flags + 0) < d) {
+      __nanosleep(256);
+      if (++spins > (1ull << 25)) __trap();
+    }
+  if (need_hi)
+    while (ld_acquire_sys(flags + 1) < d) {
+      __nanosleep(256);
+      if (++spins > (1ull << 25)) __trap();
+    }
+}
+
+// Publish "one more step completed" to both neighbours: [0] of the upper
+// neighbour's flags = my count as its lower neighbour, [1] of the lower one's.
+__global__ void k_peer_signal(unsigned long long* done, unsigned long long* lo_flags,
+                              unsigned long long* hi_flags) {
+  const unsigned long long d = *done + 1;
+  *done = d;
+  __threadfence_system();
+  if (lo_flags) st_release_sys(lo_flags + 1, d);
+  if (hi_flags) st_release_sys(hi_flags + 0, d);
+}
+
+// Copy 4 planes (plane pitch `plane` floats) to a peer buffer.
+__global__ void k_copy_planes(const float4* __restrict__ src, float4* dst, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 // vdt2 = fp32((V dt)^2) computed in fp64 (R8), in place over the

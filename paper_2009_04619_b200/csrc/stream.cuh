@@ -51,6 +51,8 @@ constexpr int SP = 3;           // u_prev/vdt2 ring stages (divides 9)
 
 struct StreamParams {
   float* out;                   // u_next buffer (= u_prev buffer), padded layout base
+  float* rlo;                   // lower neighbour's upper ghost planes (next buffer) or null
+  float* rhi;                   // upper neighbour's lower ghost planes (next buffer) or null
   int64_t pitch, plane;         // row / plane pitch in floats
   int nx, ny, nzl, nzg, zoff, w;
   int cz;                       // z-chunk length
@@ -503,6 +505,24 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             if (mask & (1u << (r * 4 + c))) optr[r * P.pitch + c] = f4get(res[r], c);
+      }
+      // fused halo exchange: edge planes also go straight into the neighbour's
+      // ghost planes over the peer mapping (plane-uniform branch)
+      float* rbase = nullptr;
+      if (z < R && P.rlo) rbase = P.rlo + (int64_t)z * P.plane;
+      else if (z >= P.nzl - R && P.rhi) rbase = P.rhi + (int64_t)(z - (P.nzl - R)) * P.plane;
+      if (rbase) {
+        float* rp = rbase + (int64_t)gy * P.pitch + gx;
+        if (full) {
+#pragma unroll
+          for (int r = 0; r < TYT; ++r) *reinterpret_cast<float4*>(rp + r * P.pitch) = res[r];
+        } else {
+#pragma unroll
+          for (int r = 0; r < TYT; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (mask & (1u << (r * 4 + c))) rp[r * P.pitch + c] = f4get(res[r], c);
+        }
       }
       optr += P.plane;
     }

@@ -190,6 +190,12 @@ struct wave_plan {
   cudaStream_t side = nullptr, cap = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  // fused peer-store halo exchange
+  bool have_peers = false;
+  wave_peers peers{};
+  unsigned long long* ddone = nullptr;     // steps completed (flag protocol)
+  bool remote = false;                     // enqueue with remote edge stores
+  cudaGraphExec_t gexec_peer[2] = {nullptr, nullptr};
 };
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -408,6 +414,12 @@ static wave_status launch_stream(wave_plan* P, const Launch& Lc, int cur, cudaSt
   const Maps& M = P->maps[Lc.ki];
   StreamParams p = Lc.p;
   p.out = P->buf[1 - cur];
+  p.rlo = p.rhi = nullptr;
+  if (P->remote) {
+    const int64_t plane = P->L.pitch_x * P->d.ny;
+    if (P->peers.lo_buf[1 - cur]) p.rlo = P->peers.lo_buf[1 - cur] + (P->peers.lo_nz + R) * plane;
+    if (P->peers.hi_buf[1 - cur]) p.rhi = P->peers.hi_buf[1 - cur];
+  }
   const dim3 grid(Lc.nblk), block(kernel_threads(Lc.ki));
   const size_t smem = kernel_smem(Lc.ki, P->d.pml_width);
   void* args[] = {(void*)&M.u[cur], (void*)&M.up[1 - cur], (void*)&M.v, (void*)&p};
@@ -458,8 +470,17 @@ static wave_status launch_naive(wave_plan* P, int cur, int z0, int z1, cudaStrea
 static wave_status launch_source(wave_plan* P, int cur, cudaStream_t s) {
   if (!P->src_set || !P->src_local || P->ninc == 0) return WAVE_OK;
   const int64_t k = P->sk - P->d.z_offset;
-  const int64_t off = (k + R) * P->L.pitch_x * P->d.ny + P->sj * P->L.pitch_x + P->si;
-  k_source<<<1, 1, 0, s>>>(P->buf[1 - cur], off, P->inc_d, P->ninc, P->dstep);
+  const int64_t plane = P->L.pitch_x * P->d.ny;
+  const int64_t off = (k + R) * plane + P->sj * P->L.pitch_x + P->si;
+  float* mirror = nullptr;   // the source cell in a neighbour's ghost planes (fused exchange)
+  if (P->remote) {
+    const int64_t cell = P->sj * P->L.pitch_x + P->si;
+    if (k < R && P->peers.lo_buf[1 - cur])
+      mirror = P->peers.lo_buf[1 - cur] + (P->peers.lo_nz + R + k) * plane + cell;
+    else if (k >= P->d.nz - R && P->peers.hi_buf[1 - cur])
+      mirror = P->peers.hi_buf[1 - cur] + (k - (P->d.nz - R)) * plane + cell;
+  }
+  k_source<<<1, 1, 0, s>>>(P->buf[1 - cur], off, P->inc_d, P->ninc, P->dstep, mirror);
   CK(cudaGetLastError());
   return WAVE_OK;
 }
@@ -525,8 +546,10 @@ static wave_status ensure_graph(wave_plan* P, int parity) {
 }
 
 static void drop_graphs(wave_plan* P) {
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 2; ++i) {
     if (P->gexec[i]) { cudaGraphExecDestroy(P->gexec[i]); P->gexec[i] = nullptr; }
+    if (P->gexec_peer[i]) { cudaGraphExecDestroy(P->gexec_peer[i]); P->gexec_peer[i] = nullptr; }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -605,6 +628,16 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, P->dev);
   if (get_encoder() != WAVE_OK) return bail(WAVE_ERR_CUDA);
   init_kernels();
+  {
+    // load every kernel now (lazy module loading can need an idle device,
+    // which never comes while a peer-wait kernel spins)
+    cudaFuncAttributes fa;
+    for (int ki = 0; ki < KI_N; ++ki) cudaFuncGetAttributes(&fa, g_k[ki].fn);
+    const void* aux[] = {(const void*)k_naive, (const void*)k_source, (const void*)k_vdt2, (const void*)k_inc,
+                         (const void*)k_stats, (const void*)k_peer_wait, (const void*)k_peer_signal,
+                         (const void*)k_copy_planes};
+    for (const void* f : aux) cudaFuncGetAttributes(&fa, f);
+  }
   if (const char* e = getenv("WAVE25_PF")) P->pf = atoi(e);
   if (const char* e = getenv("WAVE25_WALL_PRIO")) P->wall_prio = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
@@ -651,6 +684,7 @@ void wave_plan_destroy(wave_plan* P) {
   if (P->tab_d) cudaFree(P->tab_d);
   if (P->dstep) cudaFree(P->dstep);
   if (P->stats_d) cudaFree(P->stats_d);
+  if (P->ddone) cudaFree(P->ddone);
   if (P->inc_d) cudaFree(P->inc_d);
   if (P->wl_d) cudaFree(P->wl_d);
   if (P->side) cudaStreamDestroy(P->side);
@@ -857,6 +891,110 @@ wave_status wave_halo_views(const wave_plan* P, int32_t which, float** send_lo, 
   if (recv_lo) *recv_lo = b;
   if (recv_hi) *recv_hi = b + (nz + R) * plane;
   if (count) *count = R * plane;
+  return WAVE_OK;
+}
+
+static wave_status enqueue_peer_step(wave_plan* P, int cur, cudaStream_t s);
+
+static wave_status ensure_peer_graph(wave_plan* P, int par) {
+  if (P->gexec_peer[par]) return WAVE_OK;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(P->cap, cudaStreamCaptureModeThreadLocal));
+  wave_status st = enqueue_peer_step(P, par, P->cap);
+  if (st == WAVE_OK) st = enqueue_peer_step(P, 1 - par, P->cap);
+  cudaError_t e = cudaStreamEndCapture(P->cap, &g);
+  if (st != WAVE_OK) { if (g) cudaGraphDestroy(g); return st; }
+  if (e != cudaSuccess) return fail(WAVE_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&P->gexec_peer[par], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(WAVE_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+  return WAVE_OK;
+}
+
+wave_status wave_set_peers(wave_plan* P, const wave_peers* peers) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
+  drop_graphs(P);
+  if (!peers) {
+    P->have_peers = false;
+    P->peers = wave_peers{};
+    return WAVE_OK;
+  }
+  const bool lo = peers->lo_buf[0] && peers->lo_buf[1], hi = peers->hi_buf[0] && peers->hi_buf[1];
+  if ((peers->lo_buf[0] != nullptr) != (peers->lo_buf[1] != nullptr) ||
+      (peers->hi_buf[0] != nullptr) != (peers->hi_buf[1] != nullptr))
+    return fail(WAVE_ERR_CONFIG, "give both buffers of a neighbour or none");
+  if (!peers->my_flags || (lo && !peers->lo_flags) || (hi && !peers->hi_flags))
+    return fail(WAVE_ERR_CONFIG, "flag words missing");
+  if (lo && (P->d.z_offset == 0 || peers->lo_nz < R)) return fail(WAVE_ERR_CONFIG, "no lower neighbour at z_offset 0");
+  if (hi && P->d.z_offset + P->d.nz >= P->d.nz_global) return fail(WAVE_ERR_CONFIG, "no upper neighbour at the top");
+  if (P->d.kernel != WAVE_KERNEL_STREAM) return fail(WAVE_ERR_CONFIG, "peer stepping needs the stream kernels");
+  if (!P->ddone) CK(cudaMalloc(&P->ddone, sizeof(unsigned long long)));
+  CK(cudaMemset(P->ddone, 0, sizeof(unsigned long long)));
+  P->peers = *peers;
+  P->have_peers = true;
+  // instantiate both parities' 2-step graphs now, before any peer-wait kernel
+  // can be spinning on the device
+  for (int par = 0; par < 2; ++par) CKST(ensure_peer_graph(P, par));
+  return WAVE_OK;
+}
+
+static wave_status enqueue_peer_step(wave_plan* P, int cur, cudaStream_t s) {
+  const bool lo = P->peers.lo_buf[0] != nullptr, hi = P->peers.hi_buf[0] != nullptr;
+  using ull = unsigned long long;
+  k_peer_wait<<<1, 1, 0, s>>>(reinterpret_cast<const ull*>(P->peers.my_flags), P->ddone, lo ? 1 : 0, hi ? 1 : 0);
+  CK(cudaGetLastError());
+  P->remote = true;
+  wave_status st = enqueue_compute(P, 0, cur, s);
+  if (st == WAVE_OK) st = launch_source(P, cur, s);
+  P->remote = false;
+  if (st != WAVE_OK) return st;
+  k_peer_signal<<<1, 1, 0, s>>>(P->ddone, lo ? reinterpret_cast<ull*>(P->peers.lo_flags) : nullptr,
+                                hi ? reinterpret_cast<ull*>(P->peers.hi_flags) : nullptr);
+  CK(cudaGetLastError());
+  return WAVE_OK;
+}
+
+wave_status wave_step_peer(wave_plan* P, int64_t nsteps, void* stream) {
+  CKST(ready(P));
+  if (!P->have_peers) return fail(WAVE_ERR_STATE, "call wave_set_peers first");
+  if (nsteps < 0) return fail(WAVE_ERR_CONFIG, "nsteps < 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t left = nsteps;
+  if (left >= 2) {
+    const int par = P->cur;
+    CKST(ensure_peer_graph(P, par));
+    while (left >= 2) {
+      CK(cudaGraphLaunch(P->gexec_peer[par], s));
+      left -= 2;
+      P->step += 2;
+    }
+  }
+  if (left == 1) {
+    CKST(enqueue_peer_step(P, P->cur, s));
+    P->cur = 1 - P->cur;
+    P->step += 1;
+  }
+  return WAVE_OK;
+}
+
+wave_status wave_push_halo(wave_plan* P, int32_t which, void* stream) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
+  if (!P->have_peers) return fail(WAVE_ERR_STATE, "call wave_set_peers first");
+  if (which != 0 && which != 1) return fail(WAVE_ERR_CONFIG, "which must be 0 or 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int bi = which == 1 ? P->cur : 1 - P->cur;
+  const int64_t plane = P->L.pitch_x * P->d.ny, nz = P->d.nz, n4 = R * plane / 4;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n4 + 255) / 256, 4 * 148);
+  if (P->peers.lo_buf[bi]) {
+    k_copy_planes<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(P->buf[bi] + R * plane),
+                                         reinterpret_cast<float4*>(P->peers.lo_buf[bi] + (P->peers.lo_nz + R) * plane), n4);
+    CK(cudaGetLastError());
+  }
+  if (P->peers.hi_buf[bi]) {
+    k_copy_planes<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(P->buf[bi] + nz * plane),
+                                         reinterpret_cast<float4*>(P->peers.hi_buf[bi]), n4);
+    CK(cudaGetLastError());
+  }
   return WAVE_OK;
 }
 

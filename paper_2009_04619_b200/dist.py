@@ -1,6 +1,18 @@
 """z-slab domain decomposition across GPUs (not in the paper,
 which is single-GPU).
 
+Two exchange paths:
+
+* PeerSlabRunner (default): the exchange is fused into the compute.  Each
+  rank maps its neighbours' wavefield buffers and flag words (CUDA IPC over
+  NVLink / NVSwitch); the streaming kernels store the 4 edge planes of u_next
+  straight into the neighbours' ghost planes as they compute them, and
+  system-scope release/acquire step flags order consecutive steps
+  (wave_step_peer).  torch.distributed is used only to swap the IPC handles
+  at setup.
+* SlabRunner: edges -> NCCL send/recv of the 4-plane blocks (overlapped with
+  the interior kernel) -> join; the collective-library baseline.
+
 The extended domain is cut into contiguous z-slabs, one per rank (z is the
 outermost axis, so a slab face is one contiguous block of 4 planes).  Per time
 step only u^n's 4 boundary planes cross ranks: u^{n-1} and vdt2 are read at
@@ -122,3 +134,49 @@ class SlabRunner:
             self.plan.step_interior(stream=main)
             main.wait_stream(self.s_edge)
             self.plan.step_finish()
+
+
+def _share(t: torch.Tensor):
+    """Picklable CUDA IPC description of a tensor (torch's own mechanism)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+    fn, args = reduce_tensor(t)
+    return fn, args
+
+
+def _open(desc):
+    fn, args = desc
+    return fn(*args)
+
+
+class PeerSlabRunner:
+    """One rank's slab with the halo exchange fused into the compute kernels
+    (peer stores over NVLink + device-side step flags); see the module doc."""
+
+    def __init__(self, plan, rank: int, world: int, group=None):
+        self.plan, self.rank, self.world, self.group = plan, rank, world, group
+        if not hasattr(plan, "flags"):
+            plan.flags = torch.zeros(2, dtype=torch.int64, device=plan.device)
+        mine = (_share(plan.bufs[0]), _share(plan.bufs[1]), _share(plan.flags), plan.nz)
+        allv = [None] * world
+        dist.all_gather_object(allv, mine, group=group)
+        lo = allv[rank - 1] if rank > 0 else None
+        hi = allv[rank + 1] if rank < world - 1 else None
+        self._lo = (_open(lo[0]), _open(lo[1]), _open(lo[2]), lo[3]) if lo else None
+        self._hi = (_open(hi[0]), _open(hi[1]), _open(hi[2]), hi[3]) if hi else None
+        plan.set_peers(lo_bufs=self._lo[:2] if self._lo else None, hi_bufs=self._hi[:2] if self._hi else None,
+                       lo_nz=self._lo[3] if self._lo else 0, lo_flags=self._lo[2] if self._lo else None,
+                       hi_flags=self._hi[2] if self._hi else None)
+        self._barrier()
+
+    def _barrier(self):
+        torch.cuda.synchronize(self.plan.device)
+        dist.barrier(group=self.group)
+
+    def exchange_current(self) -> None:
+        """Push the current u^n edge planes into the neighbours' ghosts (once,
+        for a non-zero starting state)."""
+        self.plan.push_halo(1)
+        self._barrier()
+
+    def step(self, n: int = 1) -> None:
+        self.plan.step_peer(n)

@@ -104,6 +104,37 @@ class WavePlan:
     def step_finish(self) -> None:
         _abi.wave_step_finish(self._plan)
 
+    # ---- fused peer-store halo exchange ----------------------------------
+    def set_peers(self, lo_bufs=None, hi_bufs=None, lo_nz: int = 0, lo_flags=None, hi_flags=None) -> None:
+        """Wire the z-neighbours for step_peer: their two wavefield buffers and
+        flag words as torch tensors on any device (peer / IPC mappings); None
+        where there is no neighbour.  Allocates this plan's zeroed flag words."""
+        if not hasattr(self, "flags"):
+            self.flags = torch.zeros(2, dtype=torch.int64, device=self.device)
+        else:
+            self.flags.zero_()
+        pe = _abi.WavePeers()
+        if lo_bufs is not None:
+            pe.lo_buf[0], pe.lo_buf[1] = lo_bufs[0].data_ptr(), lo_bufs[1].data_ptr()
+            pe.lo_flags = lo_flags.data_ptr()
+        if hi_bufs is not None:
+            pe.hi_buf[0], pe.hi_buf[1] = hi_bufs[0].data_ptr(), hi_bufs[1].data_ptr()
+            pe.hi_flags = hi_flags.data_ptr()
+        pe.lo_nz = int(lo_nz)
+        pe.my_flags = self.flags.data_ptr()
+        self._peer_refs = (lo_bufs, hi_bufs, lo_flags, hi_flags)
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.device(self.device):
+            _abi.wave_set_peers(self._plan, pe)
+
+    def step_peer(self, n: int = 1, stream=None) -> None:
+        with torch.cuda.device(self.device):
+            _abi.wave_step_peer(self._plan, n, _stream_handle(stream))
+
+    def push_halo(self, which: int = 1, stream=None) -> None:
+        with torch.cuda.device(self.device):
+            _abi.wave_push_halo(self._plan, which, _stream_handle(stream))
+
     # ---- outputs --------------------------------------------------------
     def _buffer_view(self, ptr: int) -> torch.Tensor:
         L = self.layout

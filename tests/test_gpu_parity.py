@@ -388,3 +388,100 @@ def test_kernel_variants_bitwise(env):
     got = subprocess.run([sys.executable, "-c", VARIANT_SCRIPT, root], env={**base, **env},
                          capture_output=True, text=True, check=True).stdout
     assert ref.count("\n") == 2 and got == ref
+
+
+@pytest.mark.parametrize("nslab", [2, 3])
+def test_peer_store_slabs_one_process_bitwise(nslab):
+    # fused halo exchange: edge planes stored straight into the neighbours'
+    # ghost planes by the stencil kernels, device-side step flags; each slab
+    # stepped on its own stream == the single-plan run, bitwise
+    from paper_2009_04619_b200.dist import slab_bounds
+    s = synth.scenario("RAGGED")
+    sh = (s.nz, s.ny, s.nx)
+    u0, um1 = synth.random_state(sh, 51), synth.random_state(sh, 52)
+    V = synth.velocity(s)
+    steps = 23
+    wl = synth.wavelet_for(s, steps)
+    plans = []
+    for r in range(nslab):
+        off, nzl = slab_bounds(s.nz, r, nslab)
+        p = WavePlan(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
+        p.set_velocity(V[off:off + nzl])
+        p.set_source(*s.source, wl)
+        p.set_state(um1[off:off + nzl], u0[off:off + nzl])
+        p.flags = torch.zeros(2, dtype=torch.int64, device="cuda")
+        plans.append(p)
+    for r, p in enumerate(plans):
+        lo = plans[r - 1] if r > 0 else None
+        hi = plans[r + 1] if r < nslab - 1 else None
+        p.set_peers(lo_bufs=lo.bufs if lo else None, hi_bufs=hi.bufs if hi else None,
+                    lo_nz=lo.nz if lo else 0, lo_flags=lo.flags if lo else None,
+                    hi_flags=hi.flags if hi else None)
+    for p in plans:
+        p.push_halo(1)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in plans]
+    for p, st in zip(plans, streams):
+        p.step_peer(steps, stream=st)
+    torch.cuda.synchronize()
+    got = np.concatenate([p.read(0).cpu().numpy() for p in plans], axis=0)
+    ref, _ = run_gpu(s, steps, u0, um1, wl=wl)
+    for p in plans:
+        p.close()
+    assert np.array_equal(got, ref)
+
+
+def _peer_worker(rank, world, port, steps, q):
+    import os
+    import torch.distributed as dist
+    from paper_2009_04619_b200.dist import PeerSlabRunner, slab_bounds
+    from paper_2009_04619_b200.wave import WavePlan as WP
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        s = synth.scenario("RAGGED")
+        sh = (s.nz, s.ny, s.nx)
+        u0, um1 = synth.random_state(sh, 61), synth.random_state(sh, 62)
+        off, nzl = slab_bounds(s.nz, rank, world)
+        p = WP(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
+        p.set_velocity(synth.velocity(s)[off:off + nzl])
+        p.set_source(*s.source, synth.wavelet_for(s, steps))
+        p.set_state(um1[off:off + nzl], u0[off:off + nzl])
+        runner = PeerSlabRunner(p, rank, world)
+        runner.exchange_current()
+        runner.step(steps)
+        torch.cuda.synchronize()
+        q.put((rank, p.read(0).cpu().numpy()))
+        dist.barrier()            # keep buffers mapped until every rank is done
+        p.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_slab_runner_two_processes_bitwise():
+    # the production multi-GPU path (IPC-mapped neighbour buffers, peer stores,
+    # device flags) with 2 processes sharing one GPU == the single-plan run
+    import socket
+    import torch.multiprocessing as mp
+    steps = 19
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, steps, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    parts = sorted(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    got = np.concatenate([a for _, a in parts], axis=0)
+    s = synth.scenario("RAGGED")
+    sh = (s.nz, s.ny, s.nx)
+    ref, _ = run_gpu(s, steps, synth.random_state(sh, 61), synth.random_state(sh, 62),
+                     wl=synth.wavelet_for(s, steps))
+    assert np.array_equal(got, ref)
