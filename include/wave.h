@@ -68,8 +68,13 @@ typedef enum { WAVE_MEM_HOST = 0, WAVE_MEM_DEVICE = 1 } wave_mem;
  * path: TMA-fed z-streaming interior kernel + PML wall kernels + source
  * kernel.  NAIVE is one thread per point with all 25 loads from global memory
  * (the paper's gmem code shape), kept as an ablation /
- * debugging path; both compute bitwise-identical values. */
-typedef enum { WAVE_KERNEL_STREAM = 0, WAVE_KERNEL_NAIVE = 1 } wave_kernel;
+ * debugging path.  TB2 is two-step temporal blocking (the paper's future
+ * work): one interior launch advances two time
+ * steps reading u^n, u^{n-1}, vdt2 once (10 B per point-step instead of 16);
+ * it needs two extra wavefield buffers (wave_plan_bind_aux) and a single-slab
+ * plan, and falls back to STREAM single steps otherwise (odd step counts end
+ * with one STREAM step).  All three compute bitwise-identical values. */
+typedef enum { WAVE_KERNEL_STREAM = 0, WAVE_KERNEL_NAIVE = 1, WAVE_KERNEL_TB2 = 2 } wave_kernel;
 
 /* Problem descriptor.
  *  nx, ny, nz  extended domain (inner + PML on every face) of
@@ -166,6 +171,15 @@ WAVE_API wave_status wave_plan_create(const wave_desc *desc, wave_plan **out);
  * wavefield buffers (u^0 = u^{-1} = 0) and the vdt2 buffer,
  * builds TMA descriptors, resets the step counter to 0. */
 WAVE_API wave_status wave_plan_bind(wave_plan *plan, float *u0, float *u1, float *vdt2, void *stream);
+
+/* Bind two more caller-owned DEVICE wavefield buffers (same size and
+ * alignment as u0/u1) for WAVE_KERNEL_TB2: a two-step launch reads
+ * (u^n, u^{n-1}) from two buffers and writes (u^{n+1}, u^{n+2}) to the other
+ * two, out of place (neighbouring tiles still read the old levels while the
+ * new ones are written).  Zero-fills them; call after wave_plan_bind and
+ * before setting the state.  Which buffer holds u^n afterwards is internal:
+ * use wave_read / wave_field_ptr. */
+WAVE_API wave_status wave_plan_bind_aux(wave_plan *plan, float *u2, float *u3, void *stream);
 
 /* Destroy the plan (caller synchronises its streams first). NULL is a no-op. */
 WAVE_API void wave_plan_destroy(wave_plan *plan);
@@ -287,6 +301,16 @@ WAVE_API float wave_get_dt(const wave_plan *plan);
  * accounting in benchmarks); -1 on NULL. */
 WAVE_API int32_t wave_launches_per_step(const wave_plan *plan);
 
+/* Exact number of kernel launches wave_step(plan, nsteps) enqueues from the
+ * current state (two-step pairs, plus one single step for an odd count);
+ * -1 on NULL or nsteps < 0. */
+WAVE_API int64_t wave_launches(const wave_plan *plan, int64_t nsteps);
+
+/* Time steps one interior-kernel launch advances: 2 when wave_step runs
+ * two-step temporal blocking (WAVE_KERNEL_TB2 with aux buffers bound on a
+ * plan whose geometry supports it), else 1; -1 on NULL. */
+WAVE_API int32_t wave_steps_per_launch(const wave_plan *plan);
+
 /* ---- measurement --------------------------------------------------------- */
 
 /* Kernel kinds of one time step (index into the arrays below). */
@@ -295,12 +319,17 @@ enum { WAVE_KK_INTERIOR = 0, WAVE_KK_XWALLS = 1, WAVE_KK_YWALLS = 2, WAVE_KK_SOU
 
 /* Points each kernel kind computes per step (interior column incl. z caps,
  * x walls, y walls, source = 1 if owned), for algorithmic-byte accounting
- * (16 B per point-step).  out[WAVE_KK_N]. */
+ * (16 B per point-step).  With two-step blocking the interior
+ * entry is the points of the two-step launch (it advances them two steps per
+ * launch: 20 B per point per launch) and the wall entries are the points of
+ * the two single-step wall phases of a pair divided by 2.  out[WAVE_KK_N]. */
 WAVE_API wave_status wave_kernel_points(const wave_plan *plan, int64_t *out);
 
 /* Like wave_step (same kernels and launch configurations, direct launches
  * instead of the CUDA graph) but serialized on `stream` with a CUDA event pair
- * around every kernel launch, so each pair times one kernel alone.
+ * around every kernel launch, so each pair times one kernel alone.  With
+ * two-step blocking nsteps must be even; the interior kind then counts one
+ * launch per two steps.
  * Synchronises `stream` at the end and returns
  * the summed device time of each kernel kind over the nsteps in
  * kernel_ms[WAVE_KK_N] and the number of launches of each kind in

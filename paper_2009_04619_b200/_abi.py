@@ -18,7 +18,7 @@ WAVE_OK, WAVE_ERR_CONFIG, WAVE_ERR_UNSTABLE, WAVE_ERR_VERIFY, WAVE_ERR_CUDA, WAV
 STATUS_NAMES = {0: "WAVE_OK", 1: "WAVE_ERR_CONFIG", 2: "WAVE_ERR_UNSTABLE", 3: "WAVE_ERR_VERIFY",
                 4: "WAVE_ERR_CUDA", 5: "WAVE_ERR_ALLOC", 6: "WAVE_ERR_STATE"}
 WAVE_MEM_HOST, WAVE_MEM_DEVICE = 0, 1
-WAVE_KERNEL_STREAM, WAVE_KERNEL_NAIVE = 0, 1
+WAVE_KERNEL_STREAM, WAVE_KERNEL_NAIVE, WAVE_KERNEL_TB2 = 0, 1, 2
 REGION_NAMES = ["inner", "top", "bottom", "front", "back", "left", "right"]
 
 EXPORTS = [
@@ -28,6 +28,7 @@ EXPORTS = [
     "wave_step_finish", "wave_halo_views", "wave_read", "wave_field_ptr", "wave_check_finite",
     "wave_step_index", "wave_get_dt", "wave_launches_per_step", "wave_kernel_points",
     "wave_step_profiled", "wave_set_peers", "wave_step_peer", "wave_push_halo",
+    "wave_plan_bind_aux", "wave_launches", "wave_steps_per_launch",
 ]
 KERNEL_KINDS = ["interior", "xwalls", "ywalls", "source"]
 
@@ -108,6 +109,9 @@ def lib() -> ctypes.CDLL:
                 "wave_set_peers": ([P, ctypes.POINTER(WavePeers)], i32),
                 "wave_step_peer": ([P, i64, P], i32),
                 "wave_push_halo": ([P, i32, P], i32),
+                "wave_plan_bind_aux": ([P, P, P, P], i32),
+                "wave_launches": ([P, i64], i64),
+                "wave_steps_per_launch": ([P], i32),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)
@@ -168,6 +172,18 @@ def wave_plan_create(desc: WaveDesc) -> ctypes.c_void_p:
 
 def wave_plan_bind(plan, u0: int, u1: int, vdt2: int, stream: int) -> None:
     check(lib().wave_plan_bind(plan, u0, u1, vdt2, stream))
+
+
+def wave_plan_bind_aux(plan, u2: int, u3: int, stream: int) -> None:
+    check(lib().wave_plan_bind_aux(plan, u2, u3, stream))
+
+
+def wave_launches(plan, nsteps: int) -> int:
+    return int(lib().wave_launches(plan, int(nsteps)))
+
+
+def wave_steps_per_launch(plan) -> int:
+    return int(lib().wave_steps_per_launch(plan))
 
 
 def wave_plan_destroy(plan) -> None:

@@ -78,6 +78,17 @@ __global__ void k_source(float* __restrict__ buf, int64_t off, const float* __re
   *dstep = n + 1;
 }
 
+// Source into a value computed by a wall kernel of a two-step pair:
+// buf[off] += inc[n + delta], n = the device step counter (not advanced).
+__global__ void k_source_at(float* __restrict__ buf, int64_t off, const float* __restrict__ inc, int64_t ninc,
+                            const unsigned long long* __restrict__ dstep, int delta) {
+  const unsigned long long n = *dstep + (unsigned long long)delta;
+  if (n < (unsigned long long)ninc) buf[off] = __fadd_rn(buf[off], inc[n]);
+}
+
+// advance the device step counter by `by` (after a two-step pair)
+__global__ void k_advance(unsigned long long* dstep, int by) { *dstep += (unsigned long long)by; }
+
 // ---- fused halo exchange: neighbour step flags (system scope) -------------
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
   unsigned long long v;

@@ -310,19 +310,24 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
     all_dx0 = __all_sync(0xffffffffu, all_dx0);
     all_dy0 = __all_sync(0xffffffffu, all_dy0);
     wkind = all_dx0 ? 1 : (all_dy0 ? 2 : 0);
+    // an inner point (d = 0) inside a wall region (the frames of a two-step
+    // pair reach 4 or 8 cells into the inner box) takes cg = 0, A = B = 1:
+    // ((2u - up) + v (L + 0)) / 1, bitwise the inner update (up to the sign of 0)
 #pragma unroll
     for (int r = 0; r < TYT; ++r) {
       const int dy = dist1(gy + r, P.ny, P.w);
-      cgr[r] = __fmul_rn(__fsub_rn(stab[dist1(gy + r + 1, P.ny, P.w)], stab[dist1(gy + r - 1, P.ny, P.w)]),
-                         PG.i2hy);
+      cgr[r] = dy == 0 ? 0.f
+                       : __fmul_rn(__fsub_rn(stab[dist1(gy + r + 1, P.ny, P.w)], stab[dist1(gy + r - 1, P.ny, P.w)]),
+                                   PG.i2hy);
       Ar[r] = stab[TABN + dy];
       Br[r] = stab[2 * TABN + dy];
     }
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int dx = dist1(gx + c, P.nx, P.w);
-      cgc[c] = __fmul_rn(__fsub_rn(stab[dist1(gx + c + 1, P.nx, P.w)], stab[dist1(gx + c - 1, P.nx, P.w)]),
-                         PG.i2hx);
+      cgc[c] = dx == 0 ? 0.f
+                       : __fmul_rn(__fsub_rn(stab[dist1(gx + c + 1, P.nx, P.w)], stab[dist1(gx + c - 1, P.nx, P.w)]),
+                                   PG.i2hx);
       Ac[c] = stab[TABN + dx];
       Bc[c] = stab[2 * TABN + dx];
     }

@@ -19,6 +19,8 @@
 #include "../../include/wave.h"
 #include "aux_kernels.cuh"
 #include "stream.cuh"
+#include "tb2.cuh"
+#include <map>
 
 using namespace w25;
 
@@ -140,9 +142,37 @@ static constexpr double W8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315
 static constexpr int MAX_W = 512;
 
 struct Maps {
-  CUtensorMap u[2];      // wavefield buffer b with halo box
-  CUtensorMap up[2];     // wavefield buffer b, tile box
+  CUtensorMap u[4];      // wavefield buffer b with halo box
+  CUtensorMap up[4];     // wavefield buffer b, tile box
   CUtensorMap v;         // vdt2, tile box
+};
+
+// two-step temporal-blocking kernel (tb2.cuh) variants; WAVE25_T2_TILE selects
+struct T2Info {
+  void* fn;
+  int tx, ty, nt;
+  size_t (*smem)(int w);
+  const char* name;
+};
+template <int TX, int TY>
+static T2Info t2info(const char* name) {
+  using C = T2Cfg<TX, TY>;
+  return T2Info{(void*)k_tb2<TX, TY>, TX, TY, C::NT, &C::smem_bytes, name};
+}
+static T2Info pick_t2() {
+  static const T2Info v[] = {t2info<56, 14>("56x14"), t2info<56, 16>("56x16"), t2info<56, 24>("56x24")};
+  const char* e = getenv("WAVE25_T2_TILE");
+  if (e)
+    for (const T2Info& t : v)
+      if (!strcmp(e, t.name)) return t;
+  return v[0];
+}
+
+struct T2Maps {
+  CUtensorMap u[4];      // u^n, box (TX+16, TY+16)
+  CUtensorMap up[4];     // u^{n-1}, box (TX+8, TY+8)
+  CUtensorMap v1;        // vdt2, box (TX+8, TY+8)
+  CUtensorMap v2;        // vdt2, box (TX, TY)
 };
 
 struct Launch {          // one streaming-kernel launch
@@ -158,11 +188,11 @@ struct wave_plan {
   Coef coef{};
   std::vector<float> tab_h;          // [3][w+2]
   float* tab_d = nullptr;
-  float* buf[2] = {nullptr, nullptr};
+  float* buf[4] = {nullptr, nullptr, nullptr, nullptr};
   float* vdt2 = nullptr;
-  bool bound = false, have_vel = false;
+  bool bound = false, have_vel = false, aux = false;
   float dt = 0.f;
-  int cur = 0;                       // buf[cur] holds u^n
+  int cur = 0, prv = 1;              // buf[cur] holds u^n, buf[prv] u^{n-1}
   int64_t step = 0;
   // source
   bool src_set = false, src_local = false;
@@ -189,7 +219,16 @@ struct wave_plan {
   // streams / graphs
   cudaStream_t side = nullptr, cap = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  cudaGraphExec_t gexec[16] = {};    // 2-step graphs keyed by (cur, prv)
+  // two-step temporal blocking (WAVE_KERNEL_TB2)
+  T2Info t2{};
+  T2Maps t2maps{};
+  bool t2_ok = false;                // plan geometry supports it (else single steps)
+  int occ_t2 = 1;
+  T2Params t2p{};
+  int t2_nblk = 0;
+  std::vector<Launch> wall_p1, wall_p2;  // walls: u^{n+1} on the (w+8)-frame, u^{n+2} on the (w+4)-frame
+  cudaGraphExec_t gexec2[16] = {};   // 1-pair graphs keyed by (cur, prv)
   // fused peer-store halo exchange
   bool have_peers = false;
   wave_peers peers{};
@@ -252,7 +291,7 @@ static wave_status validate(const wave_desc* d) {
     return fail(WAVE_ERR_CONFIG, "spacing must be > 0");
   if (!(d->dt >= 0.f) || !std::isfinite(d->dt)) return fail(WAVE_ERR_CONFIG, "dt must be >= 0 (0 = auto)");
   if (!(d->eta_max >= 0) || !std::isfinite(d->eta_max)) return fail(WAVE_ERR_CONFIG, "eta_max must be >= 0");
-  if (d->kernel != WAVE_KERNEL_STREAM && d->kernel != WAVE_KERNEL_NAIVE)
+  if (d->kernel != WAVE_KERNEL_STREAM && d->kernel != WAVE_KERNEL_NAIVE && d->kernel != WAVE_KERNEL_TB2)
     return fail(WAVE_ERR_CONFIG, "unknown kernel %d", d->kernel);
   if (d->dt == 0.f && (d->nz != d->nz_global)) return fail(WAVE_ERR_CONFIG, "auto dt needs a single-slab plan");
   return WAVE_OK;
@@ -301,7 +340,7 @@ static int kernel_threads(int ki) { return g_k[ki].nt; }
 static size_t kernel_smem(int ki, int w) { return g_k[ki].smem(w); }
 
 // z-chunk length minimising (waves x (chunk + warm-up)) for ncol columns over nz planes
-static int choose_cz(int64_t ncol, int nz, int resident) {
+static int choose_cz(int64_t ncol, int nz, int resident, double warm = 4.0) {
   int best = nz;
   double best_cost = 1e300;
   for (int k = 1; k <= 256; ++k) {
@@ -309,7 +348,7 @@ static int choose_cz(int64_t ncol, int nz, int resident) {
     if (cz < 8 && k > 1) break;
     const int64_t nch = (nz + cz - 1) / cz;
     const double waves = std::ceil((double)(ncol * nch) / std::max(1, resident));
-    const double cost = waves * (cz + 4.0);   // 8 warm-up planes ~ half a plane each
+    const double cost = waves * (cz + warm);   // warm-up planes cost ~ half a plane each
     if (cost < best_cost * 0.999) { best_cost = cost; best = cz; }
   }
   return best;
@@ -346,6 +385,39 @@ static wave_status build_launches(wave_plan* P) {
       add_regions(P, KI_WALLX, {{0, w, w, ny - w}, {nx - w, nx, w, ny - w}}, *sets[s], &P->launches[s]);
       add_regions(P, KI_WALLY, {{0, nx, 0, w}, {0, nx, ny - w, ny}}, *sets[s], &P->launches[s]);
     }
+  }
+  // two-step temporal blocking: interior launch over the (w+4)-shrunk inner xy
+  // box, walls in two single-step phases over frames of width w+8 and w+4
+  P->wall_p1.clear();
+  P->wall_p2.clear();
+  P->t2_ok = false;
+  if (P->d.kernel == WAVE_KERNEL_TB2 && P->d.nz == P->d.nz_global && nx >= 2 * w + 17 && ny >= 2 * w + 17) {
+    const T2Info& T = P->t2;
+    T2Params& q = P->t2p;
+    memset(&q, 0, sizeof q);
+    q.pitch = P->L.pitch_x;
+    q.plane = P->L.pitch_x * P->d.ny;
+    q.nx = nx; q.ny = ny; q.nzl = nz; q.nzg = (int)P->d.nz_global; q.zoff = 0; q.w = w;
+    q.dx0 = w + 4; q.dx1 = nx - w - 4; q.dy0 = w + 4; q.dy1 = ny - w - 4;   // u^{n+2} box
+    q.cx0 = w + 8; q.cx1 = nx - w - 8; q.cy0 = w + 8; q.cy1 = ny - w - 8;   // u^{n+1} box
+    q.ax0 = q.dx0 & ~3;
+    q.ay0 = q.dy0;
+    q.ntx = (q.dx1 - q.ax0 + T.tx - 1) / T.tx;
+    q.nty = (q.dy1 - q.ay0 + T.ty - 1) / T.ty;
+    int cz = choose_cz((int64_t)q.ntx * q.nty, nz, P->occ_t2 * P->nsm, 8.0);
+    if (const char* e = getenv("WAVE25_T2_CZ")) cz = std::max(1, std::min(nz, atoi(e)));
+    q.cz = cz;
+    q.nzc = (nz + cz - 1) / cz;
+    q.k = P->coef;
+    q.tab = P->tab_d;
+    q.sk = -1;
+    P->t2_nblk = q.ntx * q.nty * q.nzc;
+    const int f1 = w + 8, f2 = w + 4;
+    add_regions(P, KI_WALLX, {{0, f1, f1, ny - f1}, {nx - f1, nx, f1, ny - f1}}, all, &P->wall_p1);
+    add_regions(P, KI_WALLY, {{0, nx, 0, f1}, {0, nx, ny - f1, ny}}, all, &P->wall_p1);
+    add_regions(P, KI_WALLX, {{0, f2, f2, ny - f2}, {nx - f2, nx, f2, ny - f2}}, all, &P->wall_p2);
+    add_regions(P, KI_WALLY, {{0, nx, 0, f2}, {0, nx, ny - f2, ny}}, all, &P->wall_p2);
+    P->t2_ok = true;
   }
   return WAVE_OK;
 }
@@ -410,19 +482,21 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
 // ---------------------------------------------------------------------------
 // step enqueue
 // ---------------------------------------------------------------------------
-static wave_status launch_stream(wave_plan* P, const Launch& Lc, int cur, cudaStream_t s) {
+// u^n in buffer ui, u^{n-1} in buffer upi, u^{n+1} written to `out` (= buf[upi]
+// for an in-place step)
+static wave_status launch_stream(wave_plan* P, const Launch& Lc, int ui, int upi, float* out, cudaStream_t s) {
   const Maps& M = P->maps[Lc.ki];
   StreamParams p = Lc.p;
-  p.out = P->buf[1 - cur];
+  p.out = out;
   p.rlo = p.rhi = nullptr;
   if (P->remote) {
     const int64_t plane = P->L.pitch_x * P->d.ny;
-    if (P->peers.lo_buf[1 - cur]) p.rlo = P->peers.lo_buf[1 - cur] + (P->peers.lo_nz + R) * plane;
-    if (P->peers.hi_buf[1 - cur]) p.rhi = P->peers.hi_buf[1 - cur];
+    if (P->peers.lo_buf[upi]) p.rlo = P->peers.lo_buf[upi] + (P->peers.lo_nz + R) * plane;
+    if (P->peers.hi_buf[upi]) p.rhi = P->peers.hi_buf[upi];
   }
   const dim3 grid(Lc.nblk), block(kernel_threads(Lc.ki));
   const size_t smem = kernel_smem(Lc.ki, P->d.pml_width);
-  void* args[] = {(void*)&M.u[cur], (void*)&M.up[1 - cur], (void*)&M.v, (void*)&p};
+  void* args[] = {(void*)&M.u[ui], (void*)&M.up[upi], (void*)&M.v, (void*)&p};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -438,7 +512,7 @@ static wave_status launch_stream(wave_plan* P, const Launch& Lc, int cur, cudaSt
     // L2 set-aside for u^n: its lines (re-read as neighbours' halos) persist,
     // u_prev / vdt2 / u_next stream through the rest of L2
     attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[1].val.accessPolicyWindow.base_ptr = P->buf[cur];
+    attr[1].val.accessPolicyWindow.base_ptr = P->buf[ui];
     attr[1].val.accessPolicyWindow.num_bytes = std::min<size_t>(P->L.elems_u * 4, P->max_window);
     attr[1].val.accessPolicyWindow.hitRatio = P->l2_hit_ratio;
     attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
@@ -451,7 +525,7 @@ static wave_status launch_stream(wave_plan* P, const Launch& Lc, int cur, cudaSt
   return WAVE_OK;
 }
 
-static wave_status launch_naive(wave_plan* P, int cur, int z0, int z1, cudaStream_t s) {
+static wave_status launch_naive(wave_plan* P, int cur, int prv, int z0, int z1, cudaStream_t s) {
   if (z1 <= z0) return WAVE_OK;
   NaiveParams np;
   np.pitch = P->L.pitch_x;
@@ -462,12 +536,13 @@ static wave_status launch_naive(wave_plan* P, int cur, int z0, int z1, cudaStrea
   np.k = P->coef;
   np.tab = P->tab_d;
   const dim3 grid((unsigned)((P->d.nx + 31) / 32), (unsigned)((P->d.ny + 3) / 4), (unsigned)(z1 - z0));
-  k_naive<<<grid, dim3(32, 4), 0, s>>>(P->buf[cur], P->buf[1 - cur], P->vdt2, np);
+  k_naive<<<grid, dim3(32, 4), 0, s>>>(P->buf[cur], P->buf[prv], P->vdt2, np);
   CK(cudaGetLastError());
   return WAVE_OK;
 }
 
-static wave_status launch_source(wave_plan* P, int cur, cudaStream_t s) {
+// source into u^{n+1} = buf[prv] after an in-place step; advances the device step counter
+static wave_status launch_source(wave_plan* P, int prv, cudaStream_t s) {
   if (!P->src_set || !P->src_local || P->ninc == 0) return WAVE_OK;
   const int64_t k = P->sk - P->d.z_offset;
   const int64_t plane = P->L.pitch_x * P->d.ny;
@@ -475,26 +550,26 @@ static wave_status launch_source(wave_plan* P, int cur, cudaStream_t s) {
   float* mirror = nullptr;   // the source cell in a neighbour's ghost planes (fused exchange)
   if (P->remote) {
     const int64_t cell = P->sj * P->L.pitch_x + P->si;
-    if (k < R && P->peers.lo_buf[1 - cur])
-      mirror = P->peers.lo_buf[1 - cur] + (P->peers.lo_nz + R + k) * plane + cell;
-    else if (k >= P->d.nz - R && P->peers.hi_buf[1 - cur])
-      mirror = P->peers.hi_buf[1 - cur] + (k - (P->d.nz - R)) * plane + cell;
+    if (k < R && P->peers.lo_buf[prv])
+      mirror = P->peers.lo_buf[prv] + (P->peers.lo_nz + R + k) * plane + cell;
+    else if (k >= P->d.nz - R && P->peers.hi_buf[prv])
+      mirror = P->peers.hi_buf[prv] + (k - (P->d.nz - R)) * plane + cell;
   }
-  k_source<<<1, 1, 0, s>>>(P->buf[1 - cur], off, P->inc_d, P->ninc, P->dstep, mirror);
+  k_source<<<1, 1, 0, s>>>(P->buf[prv], off, P->inc_d, P->ninc, P->dstep, mirror);
   CK(cudaGetLastError());
   return WAVE_OK;
 }
 
 // which: 0 all planes, 1 edges, 2 interior
-static wave_status enqueue_compute(wave_plan* P, int which, int cur, cudaStream_t s) {
+static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cudaStream_t s) {
   if (P->d.kernel == WAVE_KERNEL_NAIVE) {
     const int nz = (int)P->d.nz;
-    if (which == 0 || (which == 1 && nz <= 2 * R)) return launch_naive(P, cur, 0, nz, s);
+    if (which == 0 || (which == 1 && nz <= 2 * R)) return launch_naive(P, cur, prv, 0, nz, s);
     if (which == 1) {
-      CKST(launch_naive(P, cur, 0, R, s));
-      return launch_naive(P, cur, nz - R, nz, s);
+      CKST(launch_naive(P, cur, prv, 0, R, s));
+      return launch_naive(P, cur, prv, nz - R, nz, s);
     }
-    return nz <= 2 * R ? WAVE_OK : launch_naive(P, cur, R, nz - R, s);
+    return nz <= 2 * R ? WAVE_OK : launch_naive(P, cur, prv, R, nz - R, s);
   }
   const std::vector<Launch>& Ls = P->launches[which];
   if (Ls.empty()) return WAVE_OK;
@@ -506,10 +581,10 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, cudaStream_
     CK(cudaEventRecord(P->ev_fork, s));
     CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     for (const Launch& L : Ls)
-      if (L.ki == KI_WALLX || L.ki == KI_WALLY) CKST(launch_stream(P, L, cur, P->side));
+      if (L.ki == KI_WALLX || L.ki == KI_WALLY) CKST(launch_stream(P, L, cur, prv, P->buf[prv], P->side));
   }
   for (const Launch& L : Ls)
-    if (L.ki != KI_WALLX && L.ki != KI_WALLY) CKST(launch_stream(P, L, cur, s));
+    if (L.ki != KI_WALLX && L.ki != KI_WALLY) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
   if (walls) {
     CK(cudaEventRecord(P->ev_join, P->side));
     CK(cudaStreamWaitEvent(s, P->ev_join, 0));
@@ -525,31 +600,149 @@ static bool source_in(const wave_plan* P, int which) {
   return which == 1 ? edge : !edge;
 }
 
-static wave_status enqueue_step(wave_plan* P, int cur, cudaStream_t s) {
-  CKST(enqueue_compute(P, 0, cur, s));
-  return launch_source(P, cur, s);
+// one in-place step: u^{n+1} into buf[prv]
+static wave_status enqueue_step(wave_plan* P, int cur, int prv, cudaStream_t s) {
+  CKST(enqueue_compute(P, 0, cur, prv, s));
+  return launch_source(P, prv, s);
 }
 
-static wave_status ensure_graph(wave_plan* P, int parity) {
-  if (P->gexec[parity]) return WAVE_OK;
+static wave_status capture(wave_plan* P, cudaGraphExec_t* out, wave_status (*body)(wave_plan*, int, int),
+                           int cur, int prv) {
   cudaGraph_t g = nullptr;
   CK(cudaStreamBeginCapture(P->cap, cudaStreamCaptureModeThreadLocal));
-  wave_status st = enqueue_step(P, parity, P->cap);
-  if (st == WAVE_OK) st = enqueue_step(P, 1 - parity, P->cap);
+  wave_status st = body(P, cur, prv);
   cudaError_t e = cudaStreamEndCapture(P->cap, &g);
   if (st != WAVE_OK) { if (g) cudaGraphDestroy(g); return st; }
   if (e != cudaSuccess) return fail(WAVE_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(e));
-  e = cudaGraphInstantiate(&P->gexec[parity], g, 0);
+  e = cudaGraphInstantiate(out, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return fail(WAVE_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
   return WAVE_OK;
 }
 
-static void drop_graphs(wave_plan* P) {
-  for (int i = 0; i < 2; ++i) {
-    if (P->gexec[i]) { cudaGraphExecDestroy(P->gexec[i]); P->gexec[i] = nullptr; }
-    if (P->gexec_peer[i]) { cudaGraphExecDestroy(P->gexec_peer[i]); P->gexec_peer[i] = nullptr; }
+static wave_status two_single_steps(wave_plan* P, int cur, int prv) {
+  CKST(enqueue_step(P, cur, prv, P->cap));
+  return enqueue_step(P, prv, cur, P->cap);
+}
+
+// a 2-step graph of single steps returns to the same (cur, prv)
+static wave_status ensure_graph(wave_plan* P, int cur, int prv) {
+  cudaGraphExec_t* g = &P->gexec[cur * 4 + prv];
+  return *g ? WAVE_OK : capture(P, g, two_single_steps, cur, prv);
+}
+
+// ---------------------------------------------------------------------------
+// two-step temporal blocking (WAVE_KERNEL_TB2, tb2.cuh)
+// ---------------------------------------------------------------------------
+static bool tb2_active(const wave_plan* P) {
+  return P->d.kernel == WAVE_KERNEL_TB2 && P->aux && P->t2_ok;
+}
+
+// the two buffers not holding (u^n, u^{n-1}): C gets u^{n+1}, D gets u^{n+2}
+static void pair_targets(int cur, int prv, int* c, int* d) {
+  int o[2], n = 0;
+  for (int b = 0; b < 4; ++b)
+    if (b != cur && b != prv) o[n++] = b;
+  *c = o[0];
+  *d = o[1];
+}
+
+static int64_t source_offset(const wave_plan* P) {
+  const int64_t k = P->sk - P->d.z_offset;
+  return (k + R) * P->L.pitch_x * P->d.ny + P->sj * P->L.pitch_x + P->si;
+}
+
+static bool source_active(const wave_plan* P) { return P->src_set && P->src_local && P->ninc > 0; }
+
+// source (x, y) inside the frame of width w + e that the pair's wall kernels compute
+static bool source_in_frame(const wave_plan* P, int e) {
+  const int64_t w = P->d.pml_width + e;
+  return !(P->si >= w && P->si < P->d.nx - w && P->sj >= w && P->sj < P->d.ny - w);
+}
+
+static wave_status launch_t2(wave_plan* P, int cur, int prv, int c, int d, cudaStream_t s) {
+  T2Params p = P->t2p;
+  p.outC = P->buf[c];
+  p.outD = P->buf[d];
+  p.si = (int)P->si;
+  p.sj = (int)P->sj;
+  p.sk = source_active(P) ? (int)(P->sk - P->d.z_offset) : -1;
+  p.dstep = P->dstep;
+  p.inc = P->inc_d;
+  p.ninc = P->ninc;
+  void* args[] = {(void*)&P->t2maps.u[cur], (void*)&P->t2maps.up[prv], (void*)&P->t2maps.v1,
+                  (void*)&P->t2maps.v2, (void*)&p};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P->t2_nblk);
+  cfg.blockDim = dim3(P->t2.nt);
+  cfg.dynamicSmemBytes = P->t2.smem(P->d.pml_width);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = P->prio_lo;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelExC(&cfg, P->t2.fn, args));
+  return WAVE_OK;
+}
+
+// One pair: (u^n = buf[cur], u^{n-1} = buf[prv]) -> (u^{n+1} = buf[c], u^{n+2} = buf[d]).
+// Interior: one k_tb2 launch.  Walls (side stream, overlapping it): u^{n+1} on
+// the (w+8)-wide frame, then u^{n+2} on the (w+4)-wide frame from it -- the
+// interior launch needs neither (it recomputes its own halo).
+static wave_status enqueue_pair(wave_plan* P, int cur, int prv, cudaStream_t s) {
+  int c, d;
+  pair_targets(cur, prv, &c, &d);
+  const bool src = source_active(P);
+  const bool sp1 = src && source_in_frame(P, 8), sp2 = src && source_in_frame(P, 4);
+  const bool walls = !P->wall_p1.empty() || !P->wall_p2.empty() || sp1 || sp2;
+  if (walls) {
+    CK(cudaEventRecord(P->ev_fork, s));
+    CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
+    for (const Launch& L : P->wall_p1) CKST(launch_stream(P, L, cur, prv, P->buf[c], P->side));
+    if (sp1) {
+      k_source_at<<<1, 1, 0, P->side>>>(P->buf[c], source_offset(P), P->inc_d, P->ninc, P->dstep, 0);
+      CK(cudaGetLastError());
+    }
+    for (const Launch& L : P->wall_p2) CKST(launch_stream(P, L, c, cur, P->buf[d], P->side));
+    if (sp2) {
+      k_source_at<<<1, 1, 0, P->side>>>(P->buf[d], source_offset(P), P->inc_d, P->ninc, P->dstep, 1);
+      CK(cudaGetLastError());
+    }
   }
+  CKST(launch_t2(P, cur, prv, c, d, s));
+  if (walls) {
+    CK(cudaEventRecord(P->ev_join, P->side));
+    CK(cudaStreamWaitEvent(s, P->ev_join, 0));
+  }
+  if (src) {
+    k_advance<<<1, 1, 0, s>>>(P->dstep, 2);
+    CK(cudaGetLastError());
+  }
+  return WAVE_OK;
+}
+
+static wave_status one_pair(wave_plan* P, int cur, int prv) { return enqueue_pair(P, cur, prv, P->cap); }
+
+static wave_status ensure_pair_graph(wave_plan* P, int cur, int prv) {
+  cudaGraphExec_t* g = &P->gexec2[cur * 4 + prv];
+  return *g ? WAVE_OK : capture(P, g, one_pair, cur, prv);
+}
+
+// kernel launches of one pair
+static int pair_launches(const wave_plan* P) {
+  const bool src = source_active(P);
+  return 1 + (int)P->wall_p1.size() + (int)P->wall_p2.size() + (src && source_in_frame(P, 8)) +
+         (src && source_in_frame(P, 4)) + src;
+}
+
+static void drop_graphs(wave_plan* P) {
+  for (int i = 0; i < 16; ++i) {
+    if (P->gexec[i]) { cudaGraphExecDestroy(P->gexec[i]); P->gexec[i] = nullptr; }
+    if (P->gexec2[i]) { cudaGraphExecDestroy(P->gexec2[i]); P->gexec2[i] = nullptr; }
+  }
+  for (int i = 0; i < 2; ++i)
+    if (P->gexec_peer[i]) { cudaGraphExecDestroy(P->gexec_peer[i]); P->gexec_peer[i] = nullptr; }
 }
 
 // ---------------------------------------------------------------------------
@@ -674,6 +867,19 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr(ki), kernel_threads(ki), sm);
     P->occ[ki] = std::max(1, occ);
   }
+  if (P->d.kernel == WAVE_KERNEL_TB2) {
+    P->t2 = pick_t2();
+    const size_t sm = P->t2.smem(P->d.pml_width);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, P->t2.fn);
+    if ((e = cudaFuncSetAttribute(P->t2.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
+      return bail(fail(WAVE_ERR_CUDA, "smem attribute (tb2): %s", cudaGetErrorString(e)));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, P->t2.fn, P->t2.nt, sm);
+    if (occ < 1) return bail(fail(WAVE_ERR_CONFIG, "two-step kernel does not fit on an SM (w = %d)", P->d.pml_width));
+    P->occ_t2 = occ;
+    for (const void* f : {(const void*)k_source_at, (const void*)k_advance}) cudaFuncGetAttributes(&fa, f);
+  }
   *out = P;
   return WAVE_OK;
 }
@@ -703,27 +909,44 @@ static wave_status refresh_tables(wave_plan* P, cudaStream_t s) {
   return WAVE_OK;
 }
 
+// TMA descriptors of wavefield buffer b for every kernel that reads it
+static wave_status encode_buffer(wave_plan* P, int b) {
+  const uint64_t pb = P->L.pitch_x * 4, plb = pb * P->d.ny;
+  for (int ki = 0; ki < KI_N; ++ki) {
+    const uint32_t TX = KTX(ki), CW = KCW(ki), TY = KTY(ki);
+    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
+    CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY));
+  }
+  if (P->d.kernel == WAVE_KERNEL_TB2) {
+    const uint32_t TX = P->t2.tx, TY = P->t2.ty;
+    CKST(encode3d(&P->t2maps.u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 4 * R, TY + 4 * R));
+    CKST(encode3d(&P->t2maps.up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
+  }
+  return WAVE_OK;
+}
+
 wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void* stream) {
   if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
   if (!u0 || !u1 || !vdt2 || u0 == u1) return fail(WAVE_ERR_CONFIG, "need two distinct wavefield buffers and vdt2");
   for (const void* p : {(const void*)u0, (const void*)u1, (const void*)vdt2})
     if (reinterpret_cast<uintptr_t>(p) % 128) return fail(WAVE_ERR_CONFIG, "buffers must be 128-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
-  P->buf[0] = u0; P->buf[1] = u1; P->vdt2 = vdt2;
+  P->buf[0] = u0; P->buf[1] = u1; P->buf[2] = P->buf[3] = nullptr; P->vdt2 = vdt2;
+  P->aux = false;
   CK(cudaMemsetAsync(u0, 0, P->L.elems_u * sizeof(float), s));
   CK(cudaMemsetAsync(u1, 0, P->L.elems_u * sizeof(float), s));
   CK(cudaMemsetAsync(vdt2, 0, P->L.elems_vdt2 * sizeof(float), s));
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
   const uint64_t pb = P->L.pitch_x * 4, plb = pb * P->d.ny;
-  for (int ki = 0; ki < KI_N; ++ki) {
-    const uint32_t TX = KTX(ki), CW = KCW(ki), TY = KTY(ki);
-    for (int b = 0; b < 2; ++b) {
-      CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
-      CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY));
-    }
-    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, CW, TY));
+  for (int ki = 0; ki < KI_N; ++ki)
+    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, KCW(ki), KTY(ki)));
+  if (P->d.kernel == WAVE_KERNEL_TB2) {
+    CKST(encode3d(&P->t2maps.v1, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, P->t2.tx + 2 * R, P->t2.ty + 2 * R));
+    CKST(encode3d(&P->t2maps.v2, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, P->t2.tx, P->t2.ty));
   }
+  for (int b = 0; b < 2; ++b) CKST(encode_buffer(P, b));
   P->cur = 0;
+  P->prv = 1;
   P->step = 0;
   P->bound = true;
   P->have_vel = false;
@@ -815,8 +1038,9 @@ wave_status wave_set_state(wave_plan* P, const float* uprev, const float* ucur, 
   if (!P->bound) return fail(WAVE_ERR_STATE, "bind buffers first");
   cudaStream_t s = (cudaStream_t)stream;
   const cudaMemcpyKind kind = where == WAVE_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-  const float* src[2] = {ucur, uprev};
-  for (int b = 0; b < 2; ++b) {
+  const float* src[4] = {ucur, uprev, nullptr, nullptr};
+  for (int b = 0; b < 4; ++b) {
+    if (!P->buf[b]) continue;
     CK(cudaMemsetAsync(P->buf[b], 0, P->L.elems_u * sizeof(float), s));
     if (src[b])
       CK(cudaMemcpy2DAsync(P->buf[b] + R * P->L.pitch_x * P->d.ny, P->L.pitch_x * 4, src[b], P->d.nx * 4,
@@ -824,6 +1048,7 @@ wave_status wave_set_state(wave_plan* P, const float* uprev, const float* ucur, 
   }
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
   P->cur = 0;
+  P->prv = 1;
   P->step = 0;
   return WAVE_OK;
 }
@@ -841,17 +1066,28 @@ wave_status wave_step(wave_plan* P, int64_t nsteps, void* stream) {
   if (P->d.nz != P->d.nz_global) return fail(WAVE_ERR_STATE, "multi-slab plan: use the split-step calls");
   cudaStream_t s = (cudaStream_t)stream;
   int64_t left = nsteps;
-  if (left >= 2) {
-    CKST(ensure_graph(P, P->cur));     // a 2-step graph returns to the same parity
+  if (left >= 2 && tb2_active(P)) {
+    while (left >= 2) {                // one graph per (cur, prv) state; a pair moves to (D, C)
+      CKST(ensure_pair_graph(P, P->cur, P->prv));
+      CK(cudaGraphLaunch(P->gexec2[P->cur * 4 + P->prv], s));
+      int c, d;
+      pair_targets(P->cur, P->prv, &c, &d);
+      P->cur = d;
+      P->prv = c;
+      left -= 2;
+      P->step += 2;
+    }
+  } else if (left >= 2) {
+    CKST(ensure_graph(P, P->cur, P->prv));     // a 2-step graph returns to the same state
     while (left >= 2) {
-      CK(cudaGraphLaunch(P->gexec[P->cur], s));
+      CK(cudaGraphLaunch(P->gexec[P->cur * 4 + P->prv], s));
       left -= 2;
       P->step += 2;
     }
   }
   if (left == 1) {
-    CKST(enqueue_step(P, P->cur, s));
-    P->cur = 1 - P->cur;
+    CKST(enqueue_step(P, P->cur, P->prv, s));
+    std::swap(P->cur, P->prv);
     P->step += 1;
   }
   return WAVE_OK;
@@ -860,22 +1096,22 @@ wave_status wave_step(wave_plan* P, int64_t nsteps, void* stream) {
 wave_status wave_step_edges(wave_plan* P, void* stream) {
   CKST(ready(P));
   cudaStream_t s = (cudaStream_t)stream;
-  CKST(enqueue_compute(P, 1, P->cur, s));
-  if (source_in(P, 1)) CKST(launch_source(P, P->cur, s));
+  CKST(enqueue_compute(P, 1, P->cur, P->prv, s));
+  if (source_in(P, 1)) CKST(launch_source(P, P->prv, s));
   return WAVE_OK;
 }
 
 wave_status wave_step_interior(wave_plan* P, void* stream) {
   CKST(ready(P));
   cudaStream_t s = (cudaStream_t)stream;
-  CKST(enqueue_compute(P, 2, P->cur, s));
-  if (source_in(P, 2)) CKST(launch_source(P, P->cur, s));
+  CKST(enqueue_compute(P, 2, P->cur, P->prv, s));
+  if (source_in(P, 2)) CKST(launch_source(P, P->prv, s));
   return WAVE_OK;
 }
 
 wave_status wave_step_finish(wave_plan* P) {
   CKST(ready(P));
-  P->cur = 1 - P->cur;
+  std::swap(P->cur, P->prv);
   P->step += 1;
   return WAVE_OK;
 }
@@ -885,7 +1121,7 @@ wave_status wave_halo_views(const wave_plan* P, int32_t which, float** send_lo, 
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
   if (which != 0 && which != 1) return fail(WAVE_ERR_CONFIG, "which must be 0 or 1");
   const int64_t plane = P->L.pitch_x * P->d.ny, nz = P->d.nz;
-  float* b = P->buf[which == 0 ? 1 - P->cur : P->cur];   // next (edges output) / current
+  float* b = P->buf[which == 0 ? P->prv : P->cur];   // next (edges output) / current
   if (send_lo) *send_lo = b + R * plane;
   if (send_hi) *send_hi = b + nz * plane;
   if (recv_lo) *recv_lo = b;
@@ -944,8 +1180,8 @@ static wave_status enqueue_peer_step(wave_plan* P, int cur, cudaStream_t s) {
   k_peer_wait<<<1, 1, 0, s>>>(reinterpret_cast<const ull*>(P->peers.my_flags), P->ddone, lo ? 1 : 0, hi ? 1 : 0);
   CK(cudaGetLastError());
   P->remote = true;
-  wave_status st = enqueue_compute(P, 0, cur, s);
-  if (st == WAVE_OK) st = launch_source(P, cur, s);
+  wave_status st = enqueue_compute(P, 0, cur, 1 - cur, s);
+  if (st == WAVE_OK) st = launch_source(P, 1 - cur, s);
   P->remote = false;
   if (st != WAVE_OK) return st;
   k_peer_signal<<<1, 1, 0, s>>>(P->ddone, lo ? reinterpret_cast<ull*>(P->peers.lo_flags) : nullptr,
@@ -971,7 +1207,7 @@ wave_status wave_step_peer(wave_plan* P, int64_t nsteps, void* stream) {
   }
   if (left == 1) {
     CKST(enqueue_peer_step(P, P->cur, s));
-    P->cur = 1 - P->cur;
+    std::swap(P->cur, P->prv);
     P->step += 1;
   }
   return WAVE_OK;
@@ -982,7 +1218,7 @@ wave_status wave_push_halo(wave_plan* P, int32_t which, void* stream) {
   if (!P->have_peers) return fail(WAVE_ERR_STATE, "call wave_set_peers first");
   if (which != 0 && which != 1) return fail(WAVE_ERR_CONFIG, "which must be 0 or 1");
   cudaStream_t s = (cudaStream_t)stream;
-  const int bi = which == 1 ? P->cur : 1 - P->cur;
+  const int bi = which == 1 ? P->cur : P->prv;
   const int64_t plane = P->L.pitch_x * P->d.ny, nz = P->d.nz, n4 = R * plane / 4;
   const unsigned blocks = (unsigned)std::min<int64_t>((n4 + 255) / 256, 4 * 148);
   if (P->peers.lo_buf[bi]) {
@@ -1002,7 +1238,7 @@ wave_status wave_read(const wave_plan* P, int32_t which, float* dst, int32_t whe
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
   if (!dst || (which != 0 && which != 1)) return fail(WAVE_ERR_CONFIG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
-  const float* b = P->buf[which == 0 ? P->cur : 1 - P->cur] + R * P->L.pitch_x * P->d.ny;
+  const float* b = P->buf[which == 0 ? P->cur : P->prv] + R * P->L.pitch_x * P->d.ny;
   CK(cudaMemcpy2DAsync(dst, P->d.nx * 4, b, P->L.pitch_x * 4, P->d.nx * 4, P->d.ny * P->d.nz,
                        where == WAVE_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
   if (where == WAVE_MEM_HOST) CK(cudaStreamSynchronize(s));
@@ -1012,7 +1248,7 @@ wave_status wave_read(const wave_plan* P, int32_t which, float* dst, int32_t whe
 wave_status wave_field_ptr(const wave_plan* P, int32_t which, float** out) {
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
   if (!out || (which != 0 && which != 1)) return fail(WAVE_ERR_CONFIG, "bad arguments");
-  *out = P->buf[which == 0 ? P->cur : 1 - P->cur] + R * P->L.pitch_x * P->d.ny;
+  *out = P->buf[which == 0 ? P->cur : P->prv] + R * P->L.pitch_x * P->d.ny;
   return WAVE_OK;
 }
 
@@ -1037,15 +1273,29 @@ float wave_get_dt(const wave_plan* P) { return P ? P->dt : 0.f; }
 // the dominant kernel and covers every point)
 static int kk_of(int ki) { return ki == KI_FUSED ? WAVE_KK_INTERIOR : ki; }
 
+static int64_t region_points(const std::vector<Launch>& Ls, int kind) {
+  int64_t n = 0;
+  for (const Launch& L : Ls)
+    if (kk_of(L.ki) == kind)
+      for (int r = 0; r < L.p.nreg; ++r) {
+        const Region& g = L.p.reg[r];
+        n += (int64_t)(g.x1 - g.x0) * (g.y1 - g.y0) * (g.z1 - g.z0);
+      }
+  return n;
+}
+
 wave_status wave_kernel_points(const wave_plan* P, int64_t* out) {
   if (!P || !out) return fail(WAVE_ERR_CONFIG, "bad arguments");
   for (int k = 0; k < WAVE_KK_N; ++k) out[k] = 0;
-  for (const Launch& L : P->launches[0])
-    for (int r = 0; r < L.p.nreg; ++r) {
-      const Region& g = L.p.reg[r];
-      out[kk_of(L.ki)] += (int64_t)(g.x1 - g.x0) * (g.y1 - g.y0) * (g.z1 - g.z0);
-    }
-  out[WAVE_KK_SOURCE] = (P->src_set && P->src_local && P->ninc > 0) ? 1 : 0;
+  if (tb2_active(P)) {
+    const T2Params& q = P->t2p;
+    out[WAVE_KK_INTERIOR] = (int64_t)(q.dx1 - q.dx0) * (q.dy1 - q.dy0) * q.nzl;
+    for (int k = WAVE_KK_XWALLS; k <= WAVE_KK_YWALLS; ++k)
+      out[k] = (region_points(P->wall_p1, k) + region_points(P->wall_p2, k)) / 2;
+  } else {
+    for (int k = 0; k < WAVE_KK_SOURCE; ++k) out[k] = region_points(P->launches[0], k);
+  }
+  out[WAVE_KK_SOURCE] = source_active(P) ? 1 : 0;
   return WAVE_OK;
 }
 
@@ -1053,7 +1303,9 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
   CKST(ready(P));
   if (nsteps < 0) return fail(WAVE_ERR_CONFIG, "nsteps < 0");
   if (P->d.nz != P->d.nz_global) return fail(WAVE_ERR_STATE, "multi-slab plan: use the split-step calls");
-  if (P->d.kernel != WAVE_KERNEL_STREAM) return fail(WAVE_ERR_STATE, "profiling needs the stream kernels");
+  if (P->d.kernel == WAVE_KERNEL_NAIVE) return fail(WAVE_ERR_STATE, "profiling needs the stream kernels");
+  const bool pairs = tb2_active(P);
+  if (pairs && nsteps % 2) return fail(WAVE_ERR_CONFIG, "two-step plans profile an even number of steps");
   cudaStream_t s = (cudaStream_t)stream;
   struct Rec { int kind; cudaEvent_t a, b; };
   std::vector<Rec> recs;
@@ -1065,21 +1317,57 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
     recs.push_back(r);
     return WAVE_OK;
   };
-  wave_status st = WAVE_OK;
-  for (int64_t n = 0; n < nsteps && st == WAVE_OK; ++n) {
-    const int cur = P->cur;
-    // serialized on `stream` so every event pair brackets one kernel alone
+  const bool src = source_active(P);
+  // every launch serialized on `stream` so every event pair brackets one kernel alone
+  for (int64_t n = 0; n < nsteps; n += pairs ? 2 : 1) {
+    const int cur = P->cur, prv = P->prv;
+    if (pairs) {
+      int c, d;
+      pair_targets(cur, prv, &c, &d);
+      for (const Launch& L : P->wall_p1) {
+        CKST(mk(kk_of(L.ki), s));
+        CKST(launch_stream(P, L, cur, prv, P->buf[c], s));
+        CK(cudaEventRecord(recs.back().b, s));
+      }
+      if (src && source_in_frame(P, 8)) {
+        CKST(mk(WAVE_KK_SOURCE, s));
+        k_source_at<<<1, 1, 0, s>>>(P->buf[c], source_offset(P), P->inc_d, P->ninc, P->dstep, 0);
+        CK(cudaEventRecord(recs.back().b, s));
+      }
+      for (const Launch& L : P->wall_p2) {
+        CKST(mk(kk_of(L.ki), s));
+        CKST(launch_stream(P, L, c, cur, P->buf[d], s));
+        CK(cudaEventRecord(recs.back().b, s));
+      }
+      if (src && source_in_frame(P, 4)) {
+        CKST(mk(WAVE_KK_SOURCE, s));
+        k_source_at<<<1, 1, 0, s>>>(P->buf[d], source_offset(P), P->inc_d, P->ninc, P->dstep, 1);
+        CK(cudaEventRecord(recs.back().b, s));
+      }
+      CKST(mk(WAVE_KK_INTERIOR, s));
+      CKST(launch_t2(P, cur, prv, c, d, s));
+      CK(cudaEventRecord(recs.back().b, s));
+      if (src) {
+        CKST(mk(WAVE_KK_SOURCE, s));
+        k_advance<<<1, 1, 0, s>>>(P->dstep, 2);
+        CK(cudaEventRecord(recs.back().b, s));
+      }
+      P->cur = d;
+      P->prv = c;
+      P->step += 2;
+      continue;
+    }
     for (const Launch& L : P->launches[0]) {
       CKST(mk(kk_of(L.ki), s));
-      CKST(launch_stream(P, L, cur, s));
+      CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
       CK(cudaEventRecord(recs.back().b, s));
     }
-    if (P->src_set && P->src_local && P->ninc > 0) {
+    if (src) {
       CKST(mk(WAVE_KK_SOURCE, s));
-      CKST(launch_source(P, cur, s));
+      CKST(launch_source(P, prv, s));
       CK(cudaEventRecord(recs.back().b, s));
     }
-    P->cur = 1 - P->cur;
+    std::swap(P->cur, P->prv);
     P->step += 1;
   }
   CK(cudaStreamSynchronize(s));
@@ -1106,8 +1394,38 @@ int32_t wave_launches_per_step(const wave_plan* P) {
   const bool split = P->d.nz != P->d.nz_global;     // slab plans step via edges + interior
   if (P->d.kernel == WAVE_KERNEL_NAIVE) n = split ? 3 : 1;
   else n = split ? (int)(P->launches[1].size() + P->launches[2].size()) : (int)P->launches[0].size();
-  if (P->src_set && P->src_local && P->ninc > 0) n += 1;
+  if (source_active(P)) n += 1;
   return n;
+}
+
+int64_t wave_launches(const wave_plan* P, int64_t nsteps) {
+  if (!P || nsteps < 0) return -1;
+  const int64_t single = wave_launches_per_step(P);
+  if (!tb2_active(P)) return single * nsteps;
+  return (nsteps / 2) * pair_launches(P) + (nsteps % 2) * single;
+}
+
+int32_t wave_steps_per_launch(const wave_plan* P) {
+  if (!P) return -1;
+  return tb2_active(P) ? 2 : 1;
+}
+
+wave_status wave_plan_bind_aux(wave_plan* P, float* u2, float* u3, void* stream) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "bind u0/u1/vdt2 first");
+  if (!u2 || !u3 || u2 == u3 || u2 == P->buf[0] || u2 == P->buf[1] || u3 == P->buf[0] || u3 == P->buf[1])
+    return fail(WAVE_ERR_CONFIG, "need two more distinct wavefield buffers");
+  for (const void* p : {(const void*)u2, (const void*)u3})
+    if (reinterpret_cast<uintptr_t>(p) % 128) return fail(WAVE_ERR_CONFIG, "buffers must be 128-byte aligned");
+  if (P->d.kernel != WAVE_KERNEL_TB2) return fail(WAVE_ERR_CONFIG, "aux buffers are for WAVE_KERNEL_TB2 plans");
+  cudaStream_t s = (cudaStream_t)stream;
+  P->buf[2] = u2;
+  P->buf[3] = u3;
+  CK(cudaMemsetAsync(u2, 0, P->L.elems_u * sizeof(float), s));
+  CK(cudaMemsetAsync(u3, 0, P->L.elems_u * sizeof(float), s));
+  for (int b = 2; b < 4; ++b) CKST(encode_buffer(P, b));
+  P->aux = true;
+  drop_graphs(P);
+  return WAVE_OK;
 }
 
 }  // extern "C"

@@ -42,14 +42,16 @@ class WavePlan:
 
     nx, ny, nz   extended extents of this plan (nz = slab planes)
     w            PML width;  h spacing (scalar or (hx, hy, hz));  dt (0 = auto)
-    eta_max      PML damping maximum (1/s);  kernel "stream" | "naive"
+    eta_max      PML damping maximum (1/s);  kernel "stream" | "naive" | "tb2"
+                 ("tb2": two-step temporal blocking, 4 wavefield buffers)
     nz_global, z_offset   slab position (defaults: single slab)
     """
 
     def __init__(self, nx, ny, nz, w, h, dt, eta_max=4.0, kernel="stream",
                  nz_global=None, z_offset=0, device=None, stream=None):
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        kern = {"stream": _abi.WAVE_KERNEL_STREAM, "naive": _abi.WAVE_KERNEL_NAIVE}[kernel]
+        kern = {"stream": _abi.WAVE_KERNEL_STREAM, "naive": _abi.WAVE_KERNEL_NAIVE,
+                "tb2": _abi.WAVE_KERNEL_TB2}[kernel]
         self.desc = _abi.make_desc(nx, ny, nz, w, h, float(np.float32(dt)), eta_max, kern,
                                    nz_global, z_offset)
         self.layout = _abi.wave_layout(self.desc)
@@ -58,11 +60,15 @@ class WavePlan:
         self._plan = None
         with torch.cuda.device(self.device):
             L = self.layout
-            self.bufs = [torch.empty(L.elems_u, dtype=torch.float32, device=self.device) for _ in range(2)]
+            nb = 4 if kern == _abi.WAVE_KERNEL_TB2 else 2
+            self.bufs = [torch.empty(L.elems_u, dtype=torch.float32, device=self.device) for _ in range(nb)]
             self.vdt2 = torch.empty(L.elems_vdt2, dtype=torch.float32, device=self.device)
             self._plan = _abi.wave_plan_create(self.desc)
             _abi.wave_plan_bind(self._plan, self.bufs[0].data_ptr(), self.bufs[1].data_ptr(),
                                 self.vdt2.data_ptr(), _stream_handle(stream))
+            if nb == 4:
+                _abi.wave_plan_bind_aux(self._plan, self.bufs[2].data_ptr(), self.bufs[3].data_ptr(),
+                                        _stream_handle(stream))
         self._keep = []
 
     # ---- inputs ---------------------------------------------------------
@@ -187,6 +193,15 @@ class WavePlan:
     @property
     def launches_per_step(self) -> int:
         return _abi.wave_launches_per_step(self._plan)
+
+    def launches(self, nsteps: int) -> int:
+        """Exact number of kernel launches step(nsteps) enqueues from the current state."""
+        return _abi.wave_launches(self._plan, nsteps)
+
+    @property
+    def steps_per_launch(self) -> int:
+        """2 when step() runs two-step temporal blocking, else 1."""
+        return _abi.wave_steps_per_launch(self._plan)
 
     def kernel_points(self) -> dict:
         return _abi.wave_kernel_points(self._plan)
