@@ -65,17 +65,23 @@ struct StreamParams {
   const float* tab;             // [3][w+2]: eta_d, A_d, B_d (d = 0..w), eta_{w+1} = 0
 };
 
-template <int TX, int CW, int TY, int TYT, int MINB = 2>
+// RA > 0: one CTA per SM with a producer WARPGROUP (4 warps, one issuing TMA)
+// that gives its registers back (setmaxnreg.dec to 24) so that the consumer
+// warpgroups can raise theirs to RA (setmaxnreg.inc) -- Blackwell/Hopper
+// warp-specialised register reallocation.  Needs NWC % 4 == 0.
+template <int TX, int CW, int TY, int TYT, int MINB = 2, int RA = 0>
 struct StreamCfg {
   static constexpr int LXW = (CW / 4) < 8 ? (CW / 4) : 8;   // float4 lanes per warp row
   static constexpr int LYW = 32 / LXW;                      // thread rows per warp
-  static constexpr int WX = (CW / 4) / LXW;                 // consumer warps across x
+  static constexpr int WX = (CW / 4 + LXW - 1) / LXW;      // consumer warps across x (the last
+                                                            // may have idle "phantom" lanes)
   static constexpr int WY = (TY / TYT) / LYW;               // consumer warps in y
   static constexpr int NWC = WX * WY;                       // consumer warps
-  static constexpr int NT = 32 * (NWC + 1);                 // + 1 producer warp
+  static constexpr int NPW = RA > 0 ? 4 : 1;                // producer warps
+  static constexpr int NT = 32 * (NWC + NPW);
   // register cap for MINB CTAs per SM: warps are placed round-robin on the 4
   // sub-partitions, each with a 16K-register file
-  static constexpr int WPS = (MINB * (NWC + 1) + 3) / 4;   // warps per sub-partition
+  static constexpr int WPS = (MINB * (NWC + NPW) + 3) / 4;  // warps per sub-partition
   static constexpr int MAXR_ = (16384 / (32 * WPS)) & ~7;
   static constexpr int MAXR = MAXR_ > 255 ? 255 : MAXR_;
   static constexpr int SW = TX + 2 * R;                     // smem u row stride (floats)
@@ -88,6 +94,8 @@ struct StreamCfg {
   static_assert(CW % 4 == 0 && CW <= TX && TX % 4 == 0, "tile widths");
   static_assert(32 % LXW == 0 && (TY / TYT) % LYW == 0 && TY % TYT == 0, "warp tiling");
   static_assert((U_STAGE * 4) % 128 == 0 && (P_STAGE * 4) % 128 == 0, "TMA smem alignment");
+  static_assert(RA == 0 || (MINB == 1 && NWC % 4 == 0 && RA % 8 == 0 &&
+                            NWC / 4 * RA + 24 <= (NWC / 4 + 1) * MAXR), "register reallocation budget");
 };
 
 struct PmlGeo { int nx, ny, nzg, w, T; float i2hx, i2hy, i2hz; };
@@ -147,13 +155,13 @@ __device__ __noinline__ float4 pml_row_call(float4 L, float4 C, float4 up, float
   return make_float4(res[0], res[1], res[2], res[3]);
 }
 
-template <int TX, int CW, int TY, int TYT, int MODE, int MINB>
-__global__ void __maxnreg__((StreamCfg<TX, CW, TY, TYT, MINB>::MAXR))
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0>
+__global__ void __maxnreg__((StreamCfg<TX, CW, TY, TYT, MINB, RA>::MAXR))
 k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1)
          const __grid_constant__ CUtensorMap tm_up,   // u^{n-1}, box (CW, TY, 1)
          const __grid_constant__ CUtensorMap tm_v,    // vdt2, box (CW, TY, 1)
          const __grid_constant__ StreamParams P) {
-  using C = StreamCfg<TX, CW, TY, TYT, MINB>;
+  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* su = reinterpret_cast<float*>(smem_raw);
   float* sup = su + SU * C::U_STAGE;
@@ -210,8 +218,9 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
   __syncthreads();
 
   // ======================= producer warp =================================
-  if (wid == C::NWC) {
-    if (lane != 0) return;
+  if (wid >= C::NWC) {
+    if (RA > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
+    if (wid != C::NWC || lane != 0) return;
     const uint64_t pol_u = P.upol ? policy_evict_normal() : policy_evict_last();  // u^n: halo re-reads
     const uint64_t pol_s = policy_evict_first();   // u^{n-1}, vdt2: streamed once
     // u plane p (local z, p >= zs-4) lives in u stage (p - zs + 4) % 9, use (p - zs + 4) / 9
@@ -255,6 +264,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
   }
 
   // ======================= consumer warps ================================
+  if (RA > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(RA) : "memory");
   const int lx = (wid % C::WX) * C::LXW + (lane % C::LXW);
   const int ly = (wid / C::WX) * C::LYW + (lane / C::LXW);
   const int gx = cx0 + 4 * lx;              // first x of my float4
@@ -272,6 +282,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (TX+8, TY+8, 1
       const int x = gx + c, y = gy + r;
       if (x >= G.x0 && x < G.x1 && y >= G.y0 && y < G.y1) mask |= 1u << (r * 4 + c);
     }
+  if (4 * lx >= CW) mask = 0;                // phantom lane beyond the computed width
   const bool full = mask == (TYT * 4 == 32 ? 0xffffffffu : ((1u << (TYT * 4)) - 1u));
   PmlGeo PG;
   PG.nx = P.nx; PG.ny = P.ny; PG.nzg = P.nzg; PG.w = P.w; PG.T = TABN;

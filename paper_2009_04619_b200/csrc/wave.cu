@@ -63,15 +63,16 @@ struct KInfo {
   const char* name;
 };
 
-template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2>
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0>
 static KInfo kinfo(const char* name) {
-  using C = StreamCfg<TX, CW, TY, TYT, MINB>;
-  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB>, TX, CW, TY, C::NT, &C::smem_bytes, name};
+  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA>;
+  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA>, TX, CW, TY, C::NT, &C::smem_bytes, name};
 }
 
 // interior-kernel variants (WAVE25_INNER_TILE selects one; default first)
 static const KInfo* inner_variants(int* n) {
   static const KInfo v[] = {
+      kinfo<248, 248, 8, 1, MODE_INNER, 1, 112>("248x8x1r"),
       kinfo<128, 128, 8, 1, MODE_INNER>("128x8x1"),
       kinfo<128, 128, 16, 1, MODE_INNER, 1>("128x16x1"),
       kinfo<64, 64, 16, 1, MODE_INNER>("64x16x1"),
@@ -79,6 +80,14 @@ static const KInfo* inner_variants(int* n) {
       kinfo<128, 128, 8, 1, MODE_NULL>("null128x8x1"),      // memory-pattern probe (wrong results!)
       kinfo<128, 128, 8, 1, MODE_FUSED>("fused128x8x1"),
       kinfo<128, 128, 16, 1, MODE_NULL, 1>("null128x16x1"),
+      kinfo<248, 248, 8, 1, MODE_INNER, 1>("248x8x1"),
+      kinfo<248, 248, 8, 2, MODE_INNER, 1>("248x8x2"),
+      kinfo<248, 248, 4, 1, MODE_INNER, 1>("248x4x1"),
+      kinfo<248, 248, 8, 2, MODE_NULL, 1>("null248x8x2"),
+      kinfo<224, 224, 4, 1, MODE_INNER, 1>("224x4x1"),
+      kinfo<224, 224, 8, 1, MODE_INNER, 1>("224x8x1"),
+      kinfo<224, 224, 4, 1, MODE_NULL, 1>("null224x4x1"),
+      kinfo<224, 224, 8, 1, MODE_NULL, 1>("null224x8x1"),
   };
   *n = (int)(sizeof v / sizeof v[0]);
   return v;
@@ -102,6 +111,8 @@ static const KInfo* wallx_variants(int* n) {
 static const KInfo* wally_variants(int* n) {
   static const KInfo v[] = {
       kinfo<64, 64, 8, 1, MODE_WALL, 3>("y64x8x1m3"),
+      kinfo<248, 248, 8, 1, MODE_WALL, 1, 112>("y248x8x1r"),
+      kinfo<128, 128, 8, 1, MODE_WALL, 3>("y128x8x1m3"),
       kinfo<128, 128, 8, 1, MODE_WALL, 1>("y128x8x1"),
       kinfo<128, 128, 8, 1, MODE_WALL, 2>("y128x8x1m2"),
       kinfo<128, 128, 16, 1, MODE_WALL, 1>("y128x16x1"),
@@ -380,10 +391,12 @@ static wave_status build_launches(wave_plan* P) {
     }
     // interior kernel: inner xy footprint, all z (z caps plane-uniform)
     add_regions(P, KI_INNER, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
-    // boundary kernels: left/right (x) walls; front/back (y) walls over full x
+    // boundary kernels: left/right (x) walls over the full y range (corners
+    // included); front/back (y) walls over the inner x range, so that their
+    // tiles line up with the interior kernel's wide tiles
     if (w > 0) {
-      add_regions(P, KI_WALLX, {{0, w, w, ny - w}, {nx - w, nx, w, ny - w}}, *sets[s], &P->launches[s]);
-      add_regions(P, KI_WALLY, {{0, nx, 0, w}, {0, nx, ny - w, ny}}, *sets[s], &P->launches[s]);
+      add_regions(P, KI_WALLX, {{0, w, 0, ny}, {nx - w, nx, 0, ny}}, *sets[s], &P->launches[s]);
+      add_regions(P, KI_WALLY, {{w, nx - w, 0, w}, {w, nx - w, ny - w, ny}}, *sets[s], &P->launches[s]);
     }
   }
   // two-step temporal blocking: interior launch over the (w+4)-shrunk inner xy
