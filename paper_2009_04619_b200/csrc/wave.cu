@@ -20,6 +20,7 @@
 #include "aux_kernels.cuh"
 #include "stream.cuh"
 #include "tb2.cuh"
+#include "paper_shapes.cuh"
 #include <map>
 
 using namespace w25;
@@ -97,6 +98,9 @@ static const KInfo* inner_variants(int* n) {
 static const KInfo* wallx_variants(int* n) {
   static const KInfo v[] = {
       kinfo<24, 16, 32, 1, MODE_WALL>("x24c16x32x1"),
+      kinfo<28, 16, 32, 1, MODE_WALL>("x28c16x32x1"),
+      kinfo<28, 16, 64, 1, MODE_WALL, 1>("x28c16x64x1"),
+      kinfo<28, 16, 32, 1, MODE_WALL, 3>("x28c16x32x1m3"),
       kinfo<24, 16, 32, 1, MODE_WALL, 3>("x24c16x32x1m3"),
       kinfo<24, 16, 32, 1, MODE_WALL, 4>("x24c16x32x1m4"),
       kinfo<32, 16, 32, 1, MODE_WALL>("x32c16x32x1"),
@@ -495,9 +499,53 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
 // ---------------------------------------------------------------------------
 // step enqueue
 // ---------------------------------------------------------------------------
+// Code-shape ablation: WAVE25_ABLATION replaces the interior
+// kernel by one of the paper's shapes (paper_shapes.cuh) over the same regions.
+static const char* ablation_shape() {
+  static const char* e = getenv("WAVE25_ABLATION");
+  return (e && *e) ? e : nullptr;
+}
+
+template <bool CHK>
+static bool launch_shape(const char* sh, const AblParams& a, int ex, int ey, int ez, cudaStream_t s) {
+  auto cdiv = [](int a_, int b_) { return (unsigned)((a_ + b_ - 1) / b_); };
+  if (!strcmp(sh, "gmem_32x4x1")) k_gmem<32, 4, 1, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 4), ez), dim3(32, 4, 1), 0, s>>>(a);
+  else if (!strcmp(sh, "gmem_8x8x8")) k_gmem<8, 8, 8, CHK><<<dim3(cdiv(ex, 8), cdiv(ey, 8), cdiv(ez, 8)), dim3(8, 8, 8), 0, s>>>(a);
+  else if (!strcmp(sh, "smem_u")) k_smem_u<CHK><<<dim3(cdiv(ex, 8), cdiv(ey, 8), cdiv(ez, 8)), dim3(8, 8, 8), 0, s>>>(a);
+  else if (!strcmp(sh, "st_smem_32x16")) k_st<ST_SMEM, 32, 16, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 16)), dim3(32, 16), 0, s>>>(a);
+  else if (!strcmp(sh, "st_reg_shft_32x16")) k_st<ST_SHFT, 32, 16, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 16)), dim3(32, 16), 0, s>>>(a);
+  else if (!strcmp(sh, "st_reg_fixed_32x16")) k_st<ST_FIXED, 32, 16, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 16)), dim3(32, 16), 0, s>>>(a);
+  else if (!strcmp(sh, "st_reg_fixed_32x32")) k_st<ST_FIXED, 32, 32, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 32)), dim3(32, 32), 0, s>>>(a);
+  else return false;
+  return true;
+}
+
+static wave_status launch_ablation(wave_plan* P, const Launch& Lc, int ui, int upi, float* out, cudaStream_t s) {
+  const char* sh = ablation_shape();
+  for (int r = 0; r < Lc.p.nreg; ++r) {
+    const Region& g = Lc.p.reg[r];
+    AblParams a;
+    a.u = P->buf[ui]; a.up = P->buf[upi]; a.out = out; a.v = P->vdt2;
+    a.pitch = P->L.pitch_x; a.plane = P->L.pitch_x * P->d.ny;
+    a.nx = (int)P->d.nx; a.ny = (int)P->d.ny; a.nzl = (int)P->d.nz; a.nzg = (int)P->d.nz_global;
+    a.zoff = (int)P->d.z_offset; a.w = P->d.pml_width;
+    a.x0 = g.x0; a.x1 = g.x1; a.y0 = g.y0; a.y1 = g.y1; a.z0 = g.z0; a.z1 = g.z1;
+    a.k = P->coef; a.tab = P->tab_d;
+    const int ex = g.x1 - g.x0, ey = g.y1 - g.y0, ez = g.z1 - g.z0;
+    if (a.w < R) {
+      if (!launch_shape<true>(sh, a, ex, ey, ez, s)) return fail(WAVE_ERR_CONFIG, "unknown WAVE25_ABLATION shape '%s'", sh);
+    } else if (!launch_shape<false>(sh, a, ex, ey, ez, s)) {
+      return fail(WAVE_ERR_CONFIG, "unknown WAVE25_ABLATION shape '%s'", sh);
+    }
+    CK(cudaGetLastError());
+  }
+  return WAVE_OK;
+}
+
 // u^n in buffer ui, u^{n-1} in buffer upi, u^{n+1} written to `out` (= buf[upi]
 // for an in-place step)
 static wave_status launch_stream(wave_plan* P, const Launch& Lc, int ui, int upi, float* out, cudaStream_t s) {
+  if (Lc.ki == KI_INNER && ablation_shape() && !P->remote) return launch_ablation(P, Lc, ui, upi, out, s);
   const Maps& M = P->maps[Lc.ki];
   StreamParams p = Lc.p;
   p.out = out;

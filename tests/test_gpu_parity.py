@@ -373,6 +373,9 @@ for name in ("RAGGED", "C1"):
     {"WAVE25_INNER_TILE": "128x16x1"}, {"WAVE25_INNER_TILE": "64x16x1"},
     {"WAVE25_INNER_TILE": "128x8x1"}, {"WAVE25_INNER_TILE": "248x8x1"}, {"WAVE25_INNER_TILE": "224x8x1"},
     {"WAVE25_INNER_TILE": "248x8x2"},
+    {"WAVE25_ABLATION": "gmem_32x4x1"}, {"WAVE25_ABLATION": "gmem_8x8x8"}, {"WAVE25_ABLATION": "smem_u"},
+    {"WAVE25_ABLATION": "st_smem_32x16"}, {"WAVE25_ABLATION": "st_reg_shft_32x16"},
+    {"WAVE25_ABLATION": "st_reg_fixed_32x16"}, {"WAVE25_ABLATION": "st_reg_fixed_32x32"},
     {"WAVE25_WALLX_TILE": "x32c16x32x1"}, {"WAVE25_WALLX_TILE": "x24c16x64x1"},
     {"WAVE25_WALLY_TILE": "y128x8x1"}, {"WAVE25_WALLY_TILE": "y128x16x1"},
     {"WAVE25_FUSED": "1"}, {"WAVE25_FORK": "0", "WAVE25_PF": "0"}, {"WAVE25_CZ": "7"},
