@@ -76,6 +76,16 @@ typedef enum { WAVE_MEM_HOST = 0, WAVE_MEM_DEVICE = 1 } wave_mem;
  * with one STREAM step).  All three compute bitwise-identical values. */
 typedef enum { WAVE_KERNEL_STREAM = 0, WAVE_KERNEL_NAIVE = 1, WAVE_KERNEL_TB2 = 2 } wave_kernel;
 
+/* Arithmetic / storage precision of a plan.  FP32 (default): every constant
+ * computed in fp64 and rounded once to fp32 (R8), fp32 storage and
+ * arithmetic — the production path.  FP64 (SPEC.md L82 verification
+ * precision): constants, vdt2, source increments,
+ * wavefields and arithmetic in fp64 (the velocity model, dt and the wavelet
+ * are still given in fp32); every buffer and every wavefield array crossing
+ * the ABI (wave_set_state, wave_read, wave_field_ptr, halo views) holds
+ * doubles.  STREAM and NAIVE kernels only. */
+typedef enum { WAVE_PREC_FP32 = 0, WAVE_PREC_FP64 = 1 } wave_precision;
+
 /* Problem descriptor.
  *  nx, ny, nz  extended domain (inner + PML on every face) of
  *              THIS plan; x innermost.  nz = planes of this rank's z-slab
@@ -88,6 +98,7 @@ typedef enum { WAVE_KERNEL_STREAM = 0, WAVE_KERNEL_NAIVE = 1, WAVE_KERNEL_TB2 = 
  *              fp32(0.4 h_min / Vmax) resolved at wave_set_velocity (SPEC.md
  *              L199; single-slab plans only).  Rejected above the Courant
  *              limit dt Vmax sqrt(sum_a 1/h_a^2) <= 2/sqrt(6.5016...)
+ *  precision   wave_precision (WAVE_PREC_FP32 = 0 unless stated)
  *  eta_max     PML damping maximum (1/s), >= 0.  Default 4 (stable; SPEC's
  *              100 diverges, R5)
  *  nz_global,  this slab covers global planes [z_offset, z_offset + nz) of
@@ -99,13 +110,14 @@ typedef struct {
     int32_t kernel;
     double hx, hy, hz;
     float dt;
-    float reserved0;
+    int32_t precision;      /* wave_precision */
     double eta_max;
     int64_t nz_global, z_offset;
 } wave_desc;
 
 /* Device memory layout the caller must allocate (wave_layout).
- * Wavefield buffer: [planes][ny][pitch_x] fp32, planes = nz + 2*ghost_z;
+ * Wavefield buffer: [planes][ny][pitch_x] elements (fp32, or fp64 for fp64
+ * plans), planes = nz + 2*ghost_z;
  * element (i, j, k) (local k) lives at ((k + ghost_z)*ny + j)*pitch_x + i.
  * The ghost_z = 4 planes on each z side are the zero Dirichlet fringe
  * at the global ends and the neighbour's planes (halo) between
@@ -119,6 +131,7 @@ typedef struct {
     int64_t elems_u;      /* floats per wavefield buffer                                  */
     int64_t elems_vdt2;   /* floats in the vdt2 buffer                                    */
     int64_t align_bytes;  /* 128                                                          */
+    int64_t elem_bytes;   /* 4 (fp32 plans) or 8 (fp64 plans): buffer element size        */
 } wave_layout_info;
 
 /* One region of the paper's 7-region decomposition (PAPER.md L342-356,

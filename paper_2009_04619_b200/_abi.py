@@ -19,6 +19,7 @@ STATUS_NAMES = {0: "WAVE_OK", 1: "WAVE_ERR_CONFIG", 2: "WAVE_ERR_UNSTABLE", 3: "
                 4: "WAVE_ERR_CUDA", 5: "WAVE_ERR_ALLOC", 6: "WAVE_ERR_STATE"}
 WAVE_MEM_HOST, WAVE_MEM_DEVICE = 0, 1
 WAVE_KERNEL_STREAM, WAVE_KERNEL_NAIVE, WAVE_KERNEL_TB2 = 0, 1, 2
+WAVE_PREC_FP32, WAVE_PREC_FP64 = 0, 1
 REGION_NAMES = ["inner", "top", "bottom", "front", "back", "left", "right"]
 
 EXPORTS = [
@@ -37,14 +38,15 @@ class WaveDesc(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
                 ("pml_width", ctypes.c_int32), ("kernel", ctypes.c_int32),
                 ("hx", ctypes.c_double), ("hy", ctypes.c_double), ("hz", ctypes.c_double),
-                ("dt", ctypes.c_float), ("reserved0", ctypes.c_float),
+                ("dt", ctypes.c_float), ("precision", ctypes.c_int32),
                 ("eta_max", ctypes.c_double),
                 ("nz_global", ctypes.c_int64), ("z_offset", ctypes.c_int64)]
 
 
 class WaveLayout(ctypes.Structure):
     _fields_ = [("pitch_x", ctypes.c_int64), ("ghost_z", ctypes.c_int64), ("planes", ctypes.c_int64),
-                ("elems_u", ctypes.c_int64), ("elems_vdt2", ctypes.c_int64), ("align_bytes", ctypes.c_int64)]
+                ("elems_u", ctypes.c_int64), ("elems_vdt2", ctypes.c_int64), ("align_bytes", ctypes.c_int64),
+                ("elem_bytes", ctypes.c_int64)]
 
 
 class WaveRegion(ctypes.Structure):
@@ -127,10 +129,10 @@ def check(status: int) -> None:
 
 
 def make_desc(nx, ny, nz, pml_width, h, dt, eta_max=4.0, kernel=WAVE_KERNEL_STREAM,
-              nz_global=None, z_offset=0) -> WaveDesc:
+              nz_global=None, z_offset=0, precision=WAVE_PREC_FP32) -> WaveDesc:
     hx, hy, hz = (h, h, h) if isinstance(h, (int, float)) else tuple(h)
     return WaveDesc(int(nx), int(ny), int(nz), int(pml_width), int(kernel), float(hx), float(hy),
-                    float(hz), float(dt), 0.0, float(eta_max),
+                    float(hz), float(dt), int(precision), float(eta_max),
                     int(nz if nz_global is None else nz_global), int(z_offset))
 
 

@@ -11,54 +11,61 @@ struct NaiveParams {
   int64_t pitch, plane;
   int nx, ny, nzl, nzg, zoff, w;
   int z0;                      // first local plane of this launch (gridDim.z planes)
-  Coef k;
-  const float* tab;            // [3][w+2] eta, A, B
+  Coef k;                      // fp32 plans
+  CoefT<double> kd;            // fp64 plans
+  const void* tab;             // [3][w+2] eta, A, B (T)
 };
+
+template <typename T> __device__ __forceinline__ const CoefT<T>& naive_coef(const NaiveParams& P);
+template <> __device__ __forceinline__ const CoefT<float>& naive_coef<float>(const NaiveParams& P) { return P.k; }
+template <> __device__ __forceinline__ const CoefT<double>& naive_coef<double>(const NaiveParams& P) { return P.kd; }
 
 // One thread per point; all 25 u loads from global memory (x/y fringe by
 // bounds checks, z fringe / halo from the ghost planes).  PML-vs-inner choice
 // per point ("single kernel with conditionals").
-__global__ void __launch_bounds__(128) k_naive(const float* __restrict__ u, float* __restrict__ up,
-                                               const float* __restrict__ vdt2, const NaiveParams P) {
+template <typename T>
+__global__ void __launch_bounds__(128) k_naive(const T* __restrict__ u, T* __restrict__ up,
+                                               const T* __restrict__ vdt2, const NaiveParams P) {
   const int x = blockIdx.x * 32 + threadIdx.x;
   const int y = blockIdx.y * 4 + threadIdx.y;
   const int z = P.z0 + blockIdx.z;
   if (x >= P.nx || y >= P.ny) return;
-  auto U = [&](int i, int j, int k) -> float {
-    if (i < 0 || i >= P.nx || j < 0 || j >= P.ny) return 0.f;
+  const CoefT<T>& K = naive_coef<T>(P);
+  auto U = [&](int i, int j, int k) -> T {
+    if (i < 0 || i >= P.nx || j < 0 || j >= P.ny) return T(0);
     return u[(int64_t)(k + R) * P.plane + (int64_t)j * P.pitch + i];
   };
-  Nbr n;
+  NbrT<T> n;
 #pragma unroll
   for (int m = 1; m <= R; ++m) {
     n.xm[m - 1] = U(x - m, y, z); n.xp[m - 1] = U(x + m, y, z);
     n.ym[m - 1] = U(x, y - m, z); n.yp[m - 1] = U(x, y + m, z);
     n.zm[m - 1] = U(x, y, z - m); n.zp[m - 1] = U(x, y, z + m);
   }
-  const float uc = U(x, y, z);
+  const T uc = U(x, y, z);
   const int64_t o = (int64_t)(z + R) * P.plane + (int64_t)y * P.pitch + x;
-  const float upc = up[o];
-  const float vc = vdt2[(int64_t)z * P.ny * P.pitch + (int64_t)y * P.pitch + x];
-  const float L = lap8(P.k, uc, n);
+  const T upc = up[o];
+  const T vc = vdt2[(int64_t)z * P.ny * P.pitch + (int64_t)y * P.pitch + x];
+  const T L = lap8(K, uc, n);
   const int kg = z + P.zoff;
   const int dx = dist1(x, P.nx, P.w), dy = dist1(y, P.ny, P.w), dz = dist1(kg, P.nzg, P.w);
   const int d = max(max(dx, dy), dz);
-  float res;
+  T res;
   if (d == 0) {
     res = upd_inner(L, uc, upc, vc);
   } else {
-    const int T = P.w + 2;
-    const float* eta = P.tab;
-    const float exp_ = __ldg(eta + max(max(dist1(x + 1, P.nx, P.w), dy), dz));
-    const float exm = __ldg(eta + max(max(dist1(x - 1, P.nx, P.w), dy), dz));
-    const float eyp = __ldg(eta + max(max(dx, dist1(y + 1, P.ny, P.w)), dz));
-    const float eym = __ldg(eta + max(max(dx, dist1(y - 1, P.ny, P.w)), dz));
-    const float ezp = __ldg(eta + max(max(dx, dy), dist1(kg + 1, P.nzg, P.w)));
-    const float ezm = __ldg(eta + max(max(dx, dy), dist1(kg - 1, P.nzg, P.w)));
-    const float g = __fadd_rn(__fadd_rn(gterm(exp_, exm, n.xp[0], n.xm[0], P.k.i2h[0]),
-                                        gterm(eyp, eym, n.yp[0], n.ym[0], P.k.i2h[1])),
-                              gterm(ezp, ezm, n.zp[0], n.zm[0], P.k.i2h[2]));
-    res = upd_pml(L, g, uc, upc, vc, __ldg(P.tab + T + d), __ldg(P.tab + 2 * T + d));
+    const int TN = P.w + 2;
+    const T* eta = static_cast<const T*>(P.tab);
+    const T exp_ = __ldg(eta + max(max(dist1(x + 1, P.nx, P.w), dy), dz));
+    const T exm = __ldg(eta + max(max(dist1(x - 1, P.nx, P.w), dy), dz));
+    const T eyp = __ldg(eta + max(max(dx, dist1(y + 1, P.ny, P.w)), dz));
+    const T eym = __ldg(eta + max(max(dx, dist1(y - 1, P.ny, P.w)), dz));
+    const T ezp = __ldg(eta + max(max(dx, dy), dist1(kg + 1, P.nzg, P.w)));
+    const T ezm = __ldg(eta + max(max(dx, dy), dist1(kg - 1, P.nzg, P.w)));
+    const T g = add_rn(add_rn(gterm(exp_, exm, n.xp[0], n.xm[0], K.i2h[0]),
+                              gterm(eyp, eym, n.yp[0], n.ym[0], K.i2h[1])),
+                       gterm(ezp, ezm, n.zp[0], n.zm[0], K.i2h[2]));
+    res = upd_pml(L, g, uc, upc, vc, __ldg(eta + TN + d), __ldg(eta + 2 * TN + d));
   }
   up[o] = res;
 }
@@ -67,11 +74,12 @@ __global__ void __launch_bounds__(128) k_naive(const float* __restrict__ u, floa
 // inc[n], n = the device step counter (so replayed CUDA graphs stay correct).
 // `mirror` (or null): the same cell in a neighbour's ghost planes (fused halo
 // exchange), which must carry the injected value too.
-__global__ void k_source(float* __restrict__ buf, int64_t off, const float* __restrict__ inc,
-                         int64_t ninc, unsigned long long* __restrict__ dstep, float* mirror) {
+template <typename T>
+__global__ void k_source(T* __restrict__ buf, int64_t off, const T* __restrict__ inc,
+                         int64_t ninc, unsigned long long* __restrict__ dstep, T* mirror) {
   const unsigned long long n = *dstep;
   if (n < (unsigned long long)ninc) {
-    const float v = __fadd_rn(buf[off], inc[n]);
+    const T v = add_rn(buf[off], inc[n]);
     buf[off] = v;
     if (mirror) *mirror = v;
   }
@@ -135,24 +143,26 @@ __global__ void k_copy_planes(const float4* __restrict__ src, float4* dst, int64
     dst[i] = src[i];
 }
 
-// vdt2 = fp32((V dt)^2) computed in fp64 (R8), in place over the
-// padded-pitch buffer holding V.
-__global__ void k_vdt2(float* __restrict__ buf, int64_t pitch, int nx, int64_t rows, double dt) {
+// vdt2 = (V dt)^2 computed in fp64, rounded once to T (R8), from
+// the fp32 V in a padded-pitch buffer (in place for T = float: element by
+// element, read before write).
+template <typename T>
+__global__ void k_vdt2(T* out, const float* V, int64_t pitch, int nx, int64_t rows, double dt) {
   const int64_t n = rows * (int64_t)nx;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / nx, x = i - row * nx;
-    float* p = buf + row * pitch + x;
-    const double a = (double)(*p) * dt;
-    *p = (float)(a * a);
+    const double a = (double)V[row * pitch + x] * dt;
+    out[row * pitch + x] = (T)(a * a);
   }
 }
 
-// source increments inc[n] = fp32(vdt2[src] * w[n]) (exact product in fp64)
-__global__ void k_inc(float* __restrict__ inc, const float* __restrict__ wl, int64_t ns,
-                      const float* __restrict__ vsrc) {
+// source increments inc[n] = T(vdt2[src] * w[n]) (the product in fp64: exact
+// for fp32 operands)
+template <typename T>
+__global__ void k_inc(T* __restrict__ inc, const float* __restrict__ wl, int64_t ns, const T* __restrict__ vsrc) {
   const double vs = (double)(*vsrc);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ns; i += (int64_t)gridDim.x * blockDim.x)
-    inc[i] = (float)(vs * (double)wl[i]);
+    inc[i] = (T)(vs * (double)wl[i]);
 }
 
 struct Stats {
@@ -162,14 +172,18 @@ struct Stats {
   unsigned int pad;
 };
 
-// max|u| / min / non-finite count over a padded-pitch field.
-__global__ void k_stats(const float* __restrict__ buf, int64_t pitch, int nx, int64_t rows,
+// max|u| / min / non-finite count over a padded-pitch field (max/min
+// reported in fp32).
+template <typename T>
+__global__ void k_stats(const T* __restrict__ buf, int64_t pitch, int nx, int64_t rows,
                         int positive_required, Stats* __restrict__ out) {
   unsigned int mx = 0, mn = 0x7f7fffffu, bad = 0;
   const int64_t n = rows * (int64_t)nx;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = i / nx, x = i - row * nx;
-    const float v = buf[row * pitch + x];
+    const T vt = buf[row * pitch + x];
+    if (!isfinite(vt)) { ++bad; continue; }
+    const float v = (float)vt;
     if (!isfinite(v) || (positive_required && !(v > 0.f))) { ++bad; continue; }
     const unsigned int ab = __float_as_uint(fabsf(v));
     mx = max(mx, ab);

@@ -16,53 +16,84 @@ namespace w25 {
 
 constexpr int R = 4;         // stencil radius, PAPER.md L411-414 (R = 4)
 
-// Stencil + PML constants, fp64-computed and rounded once to fp32 on the host
-// (R8).  Passed by value as a kernel parameter (constant bank).
-struct Coef {
-  float c0;                  // c_xyz
-  float cx[R], cy[R], cz[R]; // c_am, m = 1..4
-  float i2h[3];              // 1/(2 h_a)
+// Stencil + PML constants (R8): for fp32 plans fp64-computed and
+// rounded once to fp32 on the host; for fp64 plans kept in fp64.  Passed by
+// value as a kernel parameter (constant bank).
+template <typename T>
+struct CoefT {
+  T c0;                      // c_xyz
+  T cx[R], cy[R], cz[R];     // c_am, m = 1..4
+  T i2h[3];                  // 1/(2 h_a)
 };
+using Coef = CoefT<float>;
 
 // ---------------------------------------------------------------------------
-// Per-point arithmetic (SPEC.md L140-157 semantics; fp32 with FMA)
+// Per-point arithmetic (SPEC.md L140-157 semantics; fp32 or fp64 with FMA)
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
 
 // Eq. 3: c_xyz u + sum_m c_am (u(+m) + u(-m)), pair sums
 // first (keeps mirror symmetry bitwise), axes x, y, z, m = 1..4.
-struct Nbr { float xm[R], xp[R], ym[R], yp[R], zm[R], zp[R]; };
+template <typename T>
+struct NbrT { T xm[R], xp[R], ym[R], yp[R], zm[R], zp[R]; };
+using Nbr = NbrT<float>;
 
-__device__ __forceinline__ float lap8(const Coef& k, float c, const Nbr& n) {
-  float L = __fmul_rn(k.c0, c);
+template <typename T>
+__device__ __forceinline__ T lap8(const CoefT<T>& k, T c, const NbrT<T>& n) {
+  T L = mul_rn(k.c0, c);
 #pragma unroll
-  for (int m = 0; m < R; ++m) L = __fmaf_rn(k.cx[m], __fadd_rn(n.xp[m], n.xm[m]), L);
+  for (int m = 0; m < R; ++m) L = fma_rn(k.cx[m], add_rn(n.xp[m], n.xm[m]), L);
 #pragma unroll
-  for (int m = 0; m < R; ++m) L = __fmaf_rn(k.cy[m], __fadd_rn(n.yp[m], n.ym[m]), L);
+  for (int m = 0; m < R; ++m) L = fma_rn(k.cy[m], add_rn(n.yp[m], n.ym[m]), L);
 #pragma unroll
-  for (int m = 0; m < R; ++m) L = __fmaf_rn(k.cz[m], __fadd_rn(n.zp[m], n.zm[m]), L);
+  for (int m = 0; m < R; ++m) L = fma_rn(k.cz[m], add_rn(n.zp[m], n.zm[m]), L);
   return L;
 }
 
 // inner update, Eq. 2 / SPEC.md L143: (2u - u_prev) + vdt2 L
-__device__ __forceinline__ float upd_inner(float L, float c, float up, float v) {
-  return __fmaf_rn(v, L, __fmaf_rn(2.0f, c, -up));
+template <typename T>
+__device__ __forceinline__ T upd_inner(T L, T c, T up, T v) {
+  return fma_rn(v, L, fma_rn(T(2), c, -up));
 }
 
 // one grad-eta . grad-u term: ((eta+ - eta-) / 2h) * ((u+ - u-) / 2h)
-__device__ __forceinline__ float gterm(float ep, float em, float u1p, float u1m, float i2h) {
-  return __fmul_rn(__fmul_rn(__fsub_rn(ep, em), i2h), __fmul_rn(__fsub_rn(u1p, u1m), i2h));
+template <typename T>
+__device__ __forceinline__ T gterm(T ep, T em, T u1p, T u1m, T i2h) {
+  return mul_rn(mul_rn(sub_rn(ep, em), i2h), mul_rn(sub_rn(u1p, u1m), i2h));
 }
 
 // PML update: ((2u - A u_prev) + vdt2 (L + g)) / B with a true
 // IEEE division (a reciprocal multiply drifts past the 1e-5 gate, R9).
 // 0 / B (B >= 1) is +-0 exactly; testing for it keeps quiet PML cells (u = 0
-// before the wave arrives) off the software slow path of __fdiv_rn.
-__device__ __forceinline__ float upd_pml(float L, float g, float c, float up, float v,
-                                         float A, float B) {
-  const float t = __fmaf_rn(-A, up, __fmul_rn(2.0f, c));
-  const float num = __fmaf_rn(v, __fadd_rn(L, g), t);
-  return num == 0.0f ? num : __fdiv_rn(num, B);
+// before the wave arrives) off the software slow path of the division.
+template <typename T>
+__device__ __forceinline__ T upd_pml(T L, T g, T c, T up, T v, T A, T B) {
+  const T t = fma_rn(-A, up, mul_rn(T(2), c));
+  const T num = fma_rn(v, add_rn(L, g), t);
+  return num == T(0) ? num : div_rn(num, B);
 }
+
+// 16-byte vector of the precision: 4 floats or 2 doubles per lane
+template <typename T> struct VecT;
+template <> struct VecT<float> { using V = float4; static constexpr int N = 4; };
+template <> struct VecT<double> { using V = double2; static constexpr int N = 2; };
+
+__device__ __forceinline__ float vget(const float4& v, int c) {
+  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
+__device__ __forceinline__ double vget(const double2& v, int c) { return c == 0 ? v.x : v.y; }
+template <typename T> __device__ __forceinline__ typename VecT<T>::V vmake(const T* a);
+template <> __device__ __forceinline__ float4 vmake<float>(const float* a) { return make_float4(a[0], a[1], a[2], a[3]); }
+template <> __device__ __forceinline__ double2 vmake<double>(const double* a) { return make_double2(a[0], a[1]); }
 
 // Distance (cells) to the inner box along one axis: 0 inside [w, n-w), 1..w
 // in the PML, w+1 outside the domain (eta = 0; clamped so that points of a
@@ -153,11 +184,17 @@ __device__ __forceinline__ void st_cs_f4(float* p, float4 v) {
   asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w) : "memory");
 }
+__device__ __forceinline__ void st_cs_v(float* p, float4 v) { st_cs_f4(p, v); }
+__device__ __forceinline__ void st_cs_v(double* p, double2 v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
 
 __device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
-
-__device__ __forceinline__ float f4get(const float4& v, int c) {
-  return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+template <typename T>
+__device__ __forceinline__ typename VecT<T>::V ldv(const T* p) {
+  return *reinterpret_cast<const typename VecT<T>::V*>(p);
 }
+
+__device__ __forceinline__ float f4get(const float4& v, int c) { return vget(v, c); }
 
 }  // namespace w25

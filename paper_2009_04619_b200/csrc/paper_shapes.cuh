@@ -35,7 +35,10 @@ struct AblParams {
 template <bool CHK>
 __device__ __forceinline__ float abl_u(const AblParams& P, int x, int y, int z) {
   if (CHK && (x < 0 || x >= P.nx || y < 0 || y >= P.ny)) return 0.f;     // Dirichlet fringe
-  return P.u[(int64_t)(z + R) * P.plane + (int64_t)y * P.pitch + x];
+  // L2-only load (ld.global.cg): u^n was written by other kernels of the same
+  // CUDA graph (walls on a side branch); an L1 line cached by an earlier
+  // kernel on this SM must never be hit
+  return __ldcg(P.u + (int64_t)(z + R) * P.plane + (int64_t)y * P.pitch + x);
 }
 
 // inner update or the plane-uniform z-cap PML update of one point (x, y inner),
@@ -55,8 +58,8 @@ __device__ __forceinline__ float abl_update(const AblParams& P, int kg, float L,
 __device__ __forceinline__ void abl_store(const AblParams& P, int x, int y, int z, float L, float c,
                                           const Nbr& n) {
   const int64_t o = (int64_t)(z + R) * P.plane + (int64_t)y * P.pitch + x;
-  const float upc = P.up[o];
-  const float vc = P.v[(int64_t)z * P.ny * P.pitch + (int64_t)y * P.pitch + x];
+  const float upc = __ldcg(P.up + o);
+  const float vc = __ldcg(P.v + (int64_t)z * P.ny * P.pitch + (int64_t)y * P.pitch + x);
   P.out[o] = abl_update(P, z + P.zoff, L, c, upc, vc, n.xp[0], n.xm[0], n.yp[0], n.ym[0], n.zp[0], n.zm[0]);
 }
 

@@ -123,7 +123,7 @@ __device__ __forceinline__ float4 upd_col(const T2Params& P, const float* stab, 
   if (kg < 0 || kg >= P.nzg) return make_float4(0.f, 0.f, 0.f, 0.f);
   const int T = P.w + 2;
   const int dz = dist1(kg, P.nzg, P.w);
-  CapC cc;
+  CapCT<float> cc;
   cc.ex = stab[dz];
   cc.ezp = stab[dist1(kg + 1, P.nzg, P.w)];
   cc.ezm = stab[dist1(kg - 1, P.nzg, P.w)];
@@ -131,7 +131,7 @@ __device__ __forceinline__ float4 upd_col(const T2Params& P, const float* stab, 
   cc.B = stab[2 * T + dz];
   const float4 xp = make_float4(C.y, C.z, C.w, Rf.x);
   const float4 xm = make_float4(Lf.w, C.x, C.y, C.z);
-  return cap_update(make_float4(L[0], L[1], L[2], L[3]), C, up, v, xp, xm, yp1, ym1, zp1, zm1, cc, P.k.i2h[0],
+  return cap_update<float>(make_float4(L[0], L[1], L[2], L[3]), C, up, v, xp, xm, yp1, ym1, zp1, zm1, cc, P.k.i2h[0],
                     P.k.i2h[1], P.k.i2h[2]);
 }
 
@@ -232,17 +232,20 @@ k_tb2(const __grid_constant__ CUtensorMap tm_u,    // A = u^n, box (W0, H0, 1)
       if (t + SU <= zu1) {                       // u plane t released -> plane t+9
         const int o = t - zu0;
         mbar_wait(&empty_u[o % SU], (o / SU) & 1);
+        fence_proxy_async_smem();               // generic reads before the async-proxy overwrite
         issue_u(t + SU, o % SU);
       }
       if (t >= zs - R && t + SP <= ze + R - 1) {  // step-1 plane t released -> t+3
         const int o = t - (zs - R);
         mbar_wait(&empty_p[o % SP], (o / SP) & 1);
+        fence_proxy_async_smem();
         issue_p(t + SP, o % SP);
       }
       const int tv = t - R;                      // step-2 plane tv released -> tv+3
       if (tv >= zs && tv + SP < ze) {
         const int o = tv - zs;
         mbar_wait(&empty_v[o % SP], (o / SP) & 1);
+        fence_proxy_async_smem();
         issue_v(tv + SP, o % SP);
       }
     }

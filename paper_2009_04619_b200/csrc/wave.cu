@@ -64,10 +64,11 @@ struct KInfo {
   const char* name;
 };
 
-template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0>
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0, typename T = float>
 static KInfo kinfo(const char* name) {
-  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA>;
-  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA>, TX, CW, TY, C::NT, &C::smem_bytes, name};
+  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T>;
+  // tx = width of the u TMA box minus its halo (the half width for split boxes)
+  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA, T>, C::HW, CW, TY, C::NT, &C::smem_bytes, name};
 }
 
 // interior-kernel variants (WAVE25_INNER_TILE selects one; default first)
@@ -82,6 +83,7 @@ static const KInfo* inner_variants(int* n) {
       kinfo<128, 128, 8, 1, MODE_FUSED>("fused128x8x1"),
       kinfo<128, 128, 16, 1, MODE_NULL, 1>("null128x16x1"),
       kinfo<248, 248, 8, 1, MODE_INNER, 1>("248x8x1"),
+      kinfo<256, 256, 8, 1, MODE_INNER, 1, 112>("256x8x1r"),
       kinfo<248, 248, 8, 2, MODE_INNER, 1>("248x8x2"),
       kinfo<248, 248, 4, 1, MODE_INNER, 1>("248x4x1"),
       kinfo<248, 248, 8, 2, MODE_NULL, 1>("null248x8x2"),
@@ -135,23 +137,31 @@ static KInfo pick(const KInfo* v, int n, const char* env) {
 
 enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_N = 4 };
 
-static KInfo g_k[KI_N];
+static KInfo g_k[2][KI_N];   // [precision: 0 fp32, 1 fp64][kernel kind]
 static void init_kernels() {
   static bool done = false;
   if (done) return;
   int n = 0;
   const KInfo* v = inner_variants(&n);
-  g_k[KI_INNER] = pick(v, n, "WAVE25_INNER_TILE");
+  g_k[0][KI_INNER] = pick(v, n, "WAVE25_INNER_TILE");
   v = wallx_variants(&n);
-  g_k[KI_WALLX] = pick(v, n, "WAVE25_WALLX_TILE");
+  g_k[0][KI_WALLX] = pick(v, n, "WAVE25_WALLX_TILE");
   v = wally_variants(&n);
-  g_k[KI_WALLY] = pick(v, n, "WAVE25_WALLY_TILE");
-  g_k[KI_FUSED] = kinfo<128, 128, 8, 1, MODE_FUSED>("fused128x8x1");
+  g_k[0][KI_WALLY] = pick(v, n, "WAVE25_WALLY_TILE");
+  static const KInfo fv[] = {kinfo<256, 256, 8, 1, MODE_FUSED, 1, 112>("fused256x8x1r"),
+                             kinfo<128, 128, 8, 1, MODE_FUSED>("fused128x8x1")};
+  g_k[0][KI_FUSED] = pick(fv, 2, "WAVE25_FUSED_TILE");
+  // fp64: 16-B lanes hold 2 doubles; 124 = 992 / 8 columns,
+  // u box 132 doubles; same ring / warpgroup structure as the fp32 kernels
+  g_k[1][KI_INNER] = kinfo<124, 124, 8, 1, MODE_INNER, 1, 112, double>("d124x8x1r");
+  g_k[1][KI_WALLX] = kinfo<24, 16, 32, 1, MODE_WALL, 1, 0, double>("dx24c16x32x1");
+  g_k[1][KI_WALLY] = kinfo<32, 32, 8, 1, MODE_WALL, 3, 0, double>("dy32x8x1m3");
+  g_k[1][KI_FUSED] = kinfo<64, 64, 8, 1, MODE_FUSED, 2, 0, double>("dfused64x8x1");
   done = true;
 }
-#define KTX(ki) (g_k[ki].tx)
-#define KCW(ki) (g_k[ki].cw)
-#define KTY(ki) (g_k[ki].ty)
+#define KTX(ki) (g_k[P->prec][ki].tx)
+#define KCW(ki) (g_k[P->prec][ki].cw)
+#define KTY(ki) (g_k[P->prec][ki].ty)
 
 static constexpr double W8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0};
 static constexpr int MAX_W = 512;
@@ -200,10 +210,14 @@ struct wave_plan {
   wave_desc d{};
   wave_layout_info L{};
   int dev = 0, nsm = 148;
-  Coef coef{};
-  std::vector<float> tab_h;          // [3][w+2]
-  float* tab_d = nullptr;
-  float* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  int prec = 0;                      // 0: fp32, 1: fp64 (desc.precision)
+  size_t esz = 4;                    // bytes per element
+  Coef coef{};                       // fp32 constants (rounded once)
+  CoefT<double> coefd{};             // fp64 constants (unrounded)
+  std::vector<float> tab_h;          // [3][w+2] fp32
+  std::vector<double> tab_hd;        // [3][w+2] fp64
+  void* tab_d = nullptr;
+  float* buf[4] = {nullptr, nullptr, nullptr, nullptr};   // element type by prec (float* = base address)
   float* vdt2 = nullptr;
   bool bound = false, have_vel = false, aux = false;
   float dt = 0.f;
@@ -213,7 +227,7 @@ struct wave_plan {
   bool src_set = false, src_local = false;
   int64_t si = 0, sj = 0, sk = 0;
   std::vector<float> wavelet;
-  float* inc_d = nullptr;
+  void* inc_d = nullptr;
   float* wl_d = nullptr;
   int64_t ninc = 0;
   unsigned long long* dstep = nullptr;
@@ -225,12 +239,15 @@ struct wave_plan {
   int pf = 1;                        // L2 prefetch distance (WAVE25_PF), measured best
   int prio_lo = 0, prio_hi = 0;      // stream priority range (launch attribute)
   bool wall_prio = true;             // WAVE25_WALL_PRIO=0 disables
+  bool serial = false;               // WAVE25_SERIAL=1: walls and interior on one stream (diagnostic)
   int order = 0;                     // tile order (WAVE25_ORDER)
   int l2_persist_mb = 0;             // L2 set-aside for u (WAVE25_L2MB), 0 = off
   float l2_hit_ratio = 1.f;          // WAVE25_L2HR
   size_t max_window = 0;
   int upol = 0;                      // u L2 policy (WAVE25_UPOL)
   std::vector<Launch> launches[3];   // [0] all planes, [1] edges, [2] interior
+  Maps* maps_g = nullptr;            // device copy of maps[] (WAVE25_GMAPS=1)
+  bool gmaps = false;
   // streams / graphs
   cudaStream_t side = nullptr, cap = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -252,6 +269,11 @@ struct wave_plan {
   cudaGraphExec_t gexec_peer[2] = {nullptr, nullptr};
 };
 
+// element-offset pointer into a buffer of the plan's precision
+static inline float* eo(const wave_plan* P, const void* base, int64_t elems) {
+  return reinterpret_cast<float*>(const_cast<char*>(static_cast<const char*>(base)) + elems * (int64_t)P->esz);
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
 static wave_status get_encoder() {
@@ -266,12 +288,14 @@ static wave_status get_encoder() {
 }
 
 static wave_status encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-                            uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t b0, uint32_t b1) {
+                            uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t b0, uint32_t b1,
+                            bool f64 = false) {
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+  CUresult r = g_encode(m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
+                        dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(WAVE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -306,6 +330,10 @@ static wave_status validate(const wave_desc* d) {
     return fail(WAVE_ERR_CONFIG, "spacing must be > 0");
   if (!(d->dt >= 0.f) || !std::isfinite(d->dt)) return fail(WAVE_ERR_CONFIG, "dt must be >= 0 (0 = auto)");
   if (!(d->eta_max >= 0) || !std::isfinite(d->eta_max)) return fail(WAVE_ERR_CONFIG, "eta_max must be >= 0");
+  if (d->precision != WAVE_PREC_FP32 && d->precision != WAVE_PREC_FP64)
+    return fail(WAVE_ERR_CONFIG, "unknown precision %d", d->precision);
+  if (d->precision == WAVE_PREC_FP64 && d->kernel == WAVE_KERNEL_TB2)
+    return fail(WAVE_ERR_CONFIG, "two-step blocking (TB2) is fp32 only");
   if (d->kernel != WAVE_KERNEL_STREAM && d->kernel != WAVE_KERNEL_NAIVE && d->kernel != WAVE_KERNEL_TB2)
     return fail(WAVE_ERR_CONFIG, "unknown kernel %d", d->kernel);
   if (d->dt == 0.f && (d->nz != d->nz_global)) return fail(WAVE_ERR_CONFIG, "auto dt needs a single-slab plan");
@@ -319,6 +347,31 @@ static void make_layout(const wave_desc& d, wave_layout_info* L) {
   L->elems_u = L->planes * d.ny * L->pitch_x;
   L->elems_vdt2 = d.nz * d.ny * L->pitch_x;
   L->align_bytes = 128;
+  L->elem_bytes = d.precision == WAVE_PREC_FP64 ? 8 : 4;
+}
+
+// fp64 plans: every constant in fp64, never rounded to fp32
+static void make_constants64(const wave_desc& d, float dt, CoefT<double>* k, std::vector<double>* tab) {
+  const double ih2[3] = {1.0 / (d.hx * d.hx), 1.0 / (d.hy * d.hy), 1.0 / (d.hz * d.hz)};
+  k->c0 = W8[0] * (ih2[0] + ih2[1] + ih2[2]);
+  for (int m = 1; m <= 4; ++m) {
+    k->cx[m - 1] = W8[m] * ih2[0];
+    k->cy[m - 1] = W8[m] * ih2[1];
+    k->cz[m - 1] = W8[m] * ih2[2];
+  }
+  for (int a = 0; a < 3; ++a) k->i2h[a] = 1.0 / (2.0 * (a == 0 ? d.hx : a == 1 ? d.hy : d.hz));
+  const int w = d.pml_width, T = w + 2;
+  tab->assign(3 * T, 0.0);
+  for (int dd = 0; dd <= w; ++dd) {
+    const double r = w > 0 ? (double)dd / (double)w : 0.0;
+    const double eta = d.eta_max * r * r;
+    (*tab)[dd] = eta;
+    (*tab)[T + dd] = 1.0 - eta * (double)dt;
+    (*tab)[2 * T + dd] = 1.0 + eta * (double)dt;
+  }
+  (*tab)[w + 1] = 0.0;
+  (*tab)[T + w + 1] = 1.0;
+  (*tab)[2 * T + w + 1] = 1.0;
 }
 
 // fp64 -> fp32 once (R8)
@@ -350,9 +403,9 @@ static void make_constants(const wave_desc& d, float dt, Coef* k, std::vector<fl
 // ---------------------------------------------------------------------------
 // launch planning
 // ---------------------------------------------------------------------------
-static void* kernel_ptr(int ki) { return g_k[ki].fn; }
-static int kernel_threads(int ki) { return g_k[ki].nt; }
-static size_t kernel_smem(int ki, int w) { return g_k[ki].smem(w); }
+static void* kernel_ptr(const wave_plan* P, int ki) { return g_k[P->prec][ki].fn; }
+static int kernel_threads(const wave_plan* P, int ki) { return g_k[P->prec][ki].nt; }
+static size_t kernel_smem(const wave_plan* P, int ki) { return g_k[P->prec][ki].smem(P->d.pml_width); }
 
 // z-chunk length minimising (waves x (chunk + warm-up)) for ncol columns over nz planes
 static int choose_cz(int64_t ncol, int nz, int resident, double warm = 4.0) {
@@ -426,7 +479,7 @@ static wave_status build_launches(wave_plan* P) {
     q.cz = cz;
     q.nzc = (nz + cz - 1) / cz;
     q.k = P->coef;
-    q.tab = P->tab_d;
+    q.tab = static_cast<const float*>(P->tab_d);
     q.sk = -1;
     P->t2_nblk = q.ntx * q.nty * q.nzc;
     const int f1 = w + 8, f2 = w + 4;
@@ -466,6 +519,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   p.nx = (int)P->d.nx; p.ny = (int)P->d.ny; p.nzl = (int)P->d.nz;
   p.nzg = (int)P->d.nz_global; p.zoff = (int)P->d.z_offset; p.w = P->d.pml_width;
   p.k = P->coef;
+  p.kd = P->coefd;
   p.tab = P->tab_d;
   p.cz = cz;
   p.pf = P->pf;
@@ -530,7 +584,7 @@ static wave_status launch_ablation(wave_plan* P, const Launch& Lc, int ui, int u
     a.nx = (int)P->d.nx; a.ny = (int)P->d.ny; a.nzl = (int)P->d.nz; a.nzg = (int)P->d.nz_global;
     a.zoff = (int)P->d.z_offset; a.w = P->d.pml_width;
     a.x0 = g.x0; a.x1 = g.x1; a.y0 = g.y0; a.y1 = g.y1; a.z0 = g.z0; a.z1 = g.z1;
-    a.k = P->coef; a.tab = P->tab_d;
+    a.k = P->coef; a.tab = static_cast<const float*>(P->tab_d);
     const int ex = g.x1 - g.x0, ey = g.y1 - g.y0, ez = g.z1 - g.z0;
     if (a.w < R) {
       if (!launch_shape<true>(sh, a, ex, ey, ez, s)) return fail(WAVE_ERR_CONFIG, "unknown WAVE25_ABLATION shape '%s'", sh);
@@ -545,18 +599,24 @@ static wave_status launch_ablation(wave_plan* P, const Launch& Lc, int ui, int u
 // u^n in buffer ui, u^{n-1} in buffer upi, u^{n+1} written to `out` (= buf[upi]
 // for an in-place step)
 static wave_status launch_stream(wave_plan* P, const Launch& Lc, int ui, int upi, float* out, cudaStream_t s) {
-  if (Lc.ki == KI_INNER && ablation_shape() && !P->remote) return launch_ablation(P, Lc, ui, upi, out, s);
+  if (Lc.ki == KI_INNER && ablation_shape() && !P->remote && P->prec == 0)
+    return launch_ablation(P, Lc, ui, upi, out, s);
   const Maps& M = P->maps[Lc.ki];
   StreamParams p = Lc.p;
   p.out = out;
   p.rlo = p.rhi = nullptr;
   if (P->remote) {
     const int64_t plane = P->L.pitch_x * P->d.ny;
-    if (P->peers.lo_buf[upi]) p.rlo = P->peers.lo_buf[upi] + (P->peers.lo_nz + R) * plane;
+    if (P->peers.lo_buf[upi]) p.rlo = eo(P, P->peers.lo_buf[upi], (P->peers.lo_nz + R) * plane);
     if (P->peers.hi_buf[upi]) p.rhi = P->peers.hi_buf[upi];
   }
-  const dim3 grid(Lc.nblk), block(kernel_threads(Lc.ki));
-  const size_t smem = kernel_smem(Lc.ki, P->d.pml_width);
+  const dim3 grid(Lc.nblk), block(kernel_threads(P, Lc.ki));
+  const size_t smem = kernel_smem(P, Lc.ki);
+  if (P->gmaps && P->maps_g) {
+    p.gu = &P->maps_g[Lc.ki].u[ui];
+    p.gup = &P->maps_g[Lc.ki].up[upi];
+    p.gv = &P->maps_g[Lc.ki].v;
+  }
   void* args[] = {(void*)&M.u[ui], (void*)&M.up[upi], (void*)&M.v, (void*)&p};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -582,7 +642,7 @@ static wave_status launch_stream(wave_plan* P, const Launch& Lc, int ui, int upi
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  CK(cudaLaunchKernelExC(&cfg, kernel_ptr(Lc.ki), args));
+  CK(cudaLaunchKernelExC(&cfg, kernel_ptr(P, Lc.ki), args));
   return WAVE_OK;
 }
 
@@ -595,9 +655,15 @@ static wave_status launch_naive(wave_plan* P, int cur, int prv, int z0, int z1, 
   np.nzg = (int)P->d.nz_global; np.zoff = (int)P->d.z_offset; np.w = P->d.pml_width;
   np.z0 = z0;
   np.k = P->coef;
+  np.kd = P->coefd;
   np.tab = P->tab_d;
   const dim3 grid((unsigned)((P->d.nx + 31) / 32), (unsigned)((P->d.ny + 3) / 4), (unsigned)(z1 - z0));
-  k_naive<<<grid, dim3(32, 4), 0, s>>>(P->buf[cur], P->buf[prv], P->vdt2, np);
+  if (P->prec)
+    k_naive<double><<<grid, dim3(32, 4), 0, s>>>(reinterpret_cast<const double*>(P->buf[cur]),
+                                                 reinterpret_cast<double*>(P->buf[prv]),
+                                                 reinterpret_cast<const double*>(P->vdt2), np);
+  else
+    k_naive<float><<<grid, dim3(32, 4), 0, s>>>(P->buf[cur], P->buf[prv], P->vdt2, np);
   CK(cudaGetLastError());
   return WAVE_OK;
 }
@@ -612,11 +678,17 @@ static wave_status launch_source(wave_plan* P, int prv, cudaStream_t s) {
   if (P->remote) {
     const int64_t cell = P->sj * P->L.pitch_x + P->si;
     if (k < R && P->peers.lo_buf[prv])
-      mirror = P->peers.lo_buf[prv] + (P->peers.lo_nz + R + k) * plane + cell;
+      mirror = eo(P, P->peers.lo_buf[prv], (P->peers.lo_nz + R + k) * plane + cell);
     else if (k >= P->d.nz - R && P->peers.hi_buf[prv])
-      mirror = P->peers.hi_buf[prv] + (k - (P->d.nz - R)) * plane + cell;
+      mirror = eo(P, P->peers.hi_buf[prv], (k - (P->d.nz - R)) * plane + cell);
   }
-  k_source<<<1, 1, 0, s>>>(P->buf[prv], off, P->inc_d, P->ninc, P->dstep, mirror);
+  if (P->prec)
+    k_source<double><<<1, 1, 0, s>>>(reinterpret_cast<double*>(P->buf[prv]), off,
+                                     static_cast<const double*>(P->inc_d), P->ninc, P->dstep,
+                                     reinterpret_cast<double*>(mirror));
+  else
+    k_source<float><<<1, 1, 0, s>>>(P->buf[prv], off, static_cast<const float*>(P->inc_d), P->ninc, P->dstep,
+                                    mirror);
   CK(cudaGetLastError());
   return WAVE_OK;
 }
@@ -638,6 +710,11 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cu
   // the interior kernel (stream s) run concurrently; join before the source
   bool walls = false;
   for (const Launch& L : Ls) walls |= (L.ki == KI_WALLX || L.ki == KI_WALLY);
+  if (walls && P->serial) {                 // WAVE25_SERIAL=1: everything on `s`, walls first
+    for (const Launch& L : Ls)
+      if (L.ki == KI_WALLX || L.ki == KI_WALLY) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+    walls = false;
+  }
   if (walls) {
     CK(cudaEventRecord(P->ev_fork, s));
     CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
@@ -646,6 +723,7 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cu
   }
   for (const Launch& L : Ls)
     if (L.ki != KI_WALLX && L.ki != KI_WALLY) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+  if (P->serial) return WAVE_OK;
   if (walls) {
     CK(cudaEventRecord(P->ev_join, P->side));
     CK(cudaStreamWaitEvent(s, P->ev_join, 0));
@@ -729,7 +807,7 @@ static wave_status launch_t2(wave_plan* P, int cur, int prv, int c, int d, cudaS
   p.sj = (int)P->sj;
   p.sk = source_active(P) ? (int)(P->sk - P->d.z_offset) : -1;
   p.dstep = P->dstep;
-  p.inc = P->inc_d;
+  p.inc = static_cast<const float*>(P->inc_d);
   p.ninc = P->ninc;
   void* args[] = {(void*)&P->t2maps.u[cur], (void*)&P->t2maps.up[prv], (void*)&P->t2maps.v1,
                   (void*)&P->t2maps.v2, (void*)&p};
@@ -762,12 +840,14 @@ static wave_status enqueue_pair(wave_plan* P, int cur, int prv, cudaStream_t s) 
     CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     for (const Launch& L : P->wall_p1) CKST(launch_stream(P, L, cur, prv, P->buf[c], P->side));
     if (sp1) {
-      k_source_at<<<1, 1, 0, P->side>>>(P->buf[c], source_offset(P), P->inc_d, P->ninc, P->dstep, 0);
+      k_source_at<<<1, 1, 0, P->side>>>(P->buf[c], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+                                        P->dstep, 0);
       CK(cudaGetLastError());
     }
     for (const Launch& L : P->wall_p2) CKST(launch_stream(P, L, c, cur, P->buf[d], P->side));
     if (sp2) {
-      k_source_at<<<1, 1, 0, P->side>>>(P->buf[d], source_offset(P), P->inc_d, P->ninc, P->dstep, 1);
+      k_source_at<<<1, 1, 0, P->side>>>(P->buf[d], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+                                        P->dstep, 1);
       CK(cudaGetLastError());
     }
   }
@@ -872,6 +952,8 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (!P) return fail(WAVE_ERR_ALLOC, "host allocation failed");
   P->d = *desc;
   make_layout(P->d, &P->L);
+  P->prec = desc->precision == WAVE_PREC_FP64 ? 1 : 0;
+  P->esz = P->prec ? 8 : 4;
   P->dt = desc->dt;
   auto bail = [&](wave_status st) { wave_plan_destroy(P); return st; };
   cudaError_t e = cudaGetDevice(&P->dev);
@@ -886,14 +968,18 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
     // load every kernel now (lazy module loading can need an idle device,
     // which never comes while a peer-wait kernel spins)
     cudaFuncAttributes fa;
-    for (int ki = 0; ki < KI_N; ++ki) cudaFuncGetAttributes(&fa, g_k[ki].fn);
-    const void* aux[] = {(const void*)k_naive, (const void*)k_source, (const void*)k_vdt2, (const void*)k_inc,
-                         (const void*)k_stats, (const void*)k_peer_wait, (const void*)k_peer_signal,
+    for (int ki = 0; ki < KI_N; ++ki) cudaFuncGetAttributes(&fa, g_k[P->prec][ki].fn);
+    const void* aux[] = {(const void*)k_naive<float>, (const void*)k_source<float>, (const void*)k_vdt2<float>,
+                         (const void*)k_inc<float>, (const void*)k_stats<float>, (const void*)k_naive<double>,
+                         (const void*)k_source<double>, (const void*)k_vdt2<double>, (const void*)k_inc<double>,
+                         (const void*)k_stats<double>, (const void*)k_peer_wait, (const void*)k_peer_signal,
                          (const void*)k_copy_planes};
     for (const void* f : aux) cudaFuncGetAttributes(&fa, f);
   }
   if (const char* e = getenv("WAVE25_PF")) P->pf = atoi(e);
   if (const char* e = getenv("WAVE25_WALL_PRIO")) P->wall_prio = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_SERIAL")) P->serial = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_GMAPS")) P->gmaps = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
   if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_UPOL")) P->upol = atoi(e);
@@ -911,7 +997,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>((size_t)P->l2_persist_mb << 20, (size_t)mx));
   }
   const int T = P->d.pml_width + 2;
-  if ((e = cudaMalloc(&P->tab_d, 3 * T * sizeof(float))) != cudaSuccess ||
+  if ((e = cudaMalloc(&P->tab_d, 3 * T * P->esz)) != cudaSuccess ||
       (e = cudaMalloc(&P->dstep, sizeof(unsigned long long))) != cudaSuccess ||
       (e = cudaMalloc(&P->stats_d, sizeof(Stats))) != cudaSuccess)
     return bail(fail(WAVE_ERR_ALLOC, "cudaMalloc: %s", cudaGetErrorString(e)));
@@ -921,11 +1007,11 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
       (e = cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming)) != cudaSuccess)
     return bail(fail(WAVE_ERR_CUDA, "stream/event: %s", cudaGetErrorString(e)));
   for (int ki = 0; ki < KI_N; ++ki) {
-    const size_t sm = kernel_smem(ki, P->d.pml_width);
-    if ((e = cudaFuncSetAttribute(kernel_ptr(ki), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
+    const size_t sm = kernel_smem(P, ki);
+    if ((e = cudaFuncSetAttribute(kernel_ptr(P, ki), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
       return bail(fail(WAVE_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(e)));
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr(ki), kernel_threads(ki), sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr(P, ki), kernel_threads(P, ki), sm);
     P->occ[ki] = std::max(1, occ);
   }
   if (P->d.kernel == WAVE_KERNEL_TB2) {
@@ -949,6 +1035,7 @@ void wave_plan_destroy(wave_plan* P) {
   if (!P) return;
   drop_graphs(P);
   if (P->tab_d) cudaFree(P->tab_d);
+  if (P->maps_g) cudaFree(P->maps_g);
   if (P->dstep) cudaFree(P->dstep);
   if (P->stats_d) cudaFree(P->stats_d);
   if (P->ddone) cudaFree(P->ddone);
@@ -963,7 +1050,11 @@ void wave_plan_destroy(wave_plan* P) {
 
 static wave_status refresh_tables(wave_plan* P, cudaStream_t s) {
   make_constants(P->d, P->dt, &P->coef, &P->tab_h);
-  CK(cudaMemcpyAsync(P->tab_d, P->tab_h.data(), P->tab_h.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+  make_constants64(P->d, P->dt, &P->coefd, &P->tab_hd);
+  if (P->prec)
+    CK(cudaMemcpyAsync(P->tab_d, P->tab_hd.data(), P->tab_hd.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  else
+    CK(cudaMemcpyAsync(P->tab_d, P->tab_h.data(), P->tab_h.size() * sizeof(float), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));   // tab_h is pageable host memory
   CKST(build_launches(P));
   drop_graphs(P);
@@ -972,17 +1063,28 @@ static wave_status refresh_tables(wave_plan* P, cudaStream_t s) {
 
 // TMA descriptors of wavefield buffer b for every kernel that reads it
 static wave_status encode_buffer(wave_plan* P, int b) {
-  const uint64_t pb = P->L.pitch_x * 4, plb = pb * P->d.ny;
+  const uint64_t pb = P->L.pitch_x * P->esz, plb = pb * P->d.ny;
+  const bool f64 = P->prec == 1;
   for (int ki = 0; ki < KI_N; ++ki) {
     const uint32_t TX = KTX(ki), CW = KCW(ki), TY = KTY(ki);
-    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
-    CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY));
+    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R,
+                  f64));
+    CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY, f64));
   }
   if (P->d.kernel == WAVE_KERNEL_TB2) {
     const uint32_t TX = P->t2.tx, TY = P->t2.ty;
     CKST(encode3d(&P->t2maps.u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 4 * R, TY + 4 * R));
     CKST(encode3d(&P->t2maps.up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
   }
+  return WAVE_OK;
+}
+
+// device copy of the TMA descriptors (one per kernel kind and buffer, written
+// once per bind): kernels can read them from global memory instead of from
+// their parameter block (WAVE25_GMAPS)
+static wave_status upload_maps(wave_plan* P) {
+  if (!P->maps_g) CK(cudaMalloc(&P->maps_g, sizeof(P->maps)));
+  CK(cudaMemcpy(P->maps_g, P->maps, sizeof(P->maps), cudaMemcpyHostToDevice));
   return WAVE_OK;
 }
 
@@ -994,18 +1096,19 @@ wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void
   cudaStream_t s = (cudaStream_t)stream;
   P->buf[0] = u0; P->buf[1] = u1; P->buf[2] = P->buf[3] = nullptr; P->vdt2 = vdt2;
   P->aux = false;
-  CK(cudaMemsetAsync(u0, 0, P->L.elems_u * sizeof(float), s));
-  CK(cudaMemsetAsync(u1, 0, P->L.elems_u * sizeof(float), s));
-  CK(cudaMemsetAsync(vdt2, 0, P->L.elems_vdt2 * sizeof(float), s));
+  CK(cudaMemsetAsync(u0, 0, P->L.elems_u * P->esz, s));
+  CK(cudaMemsetAsync(u1, 0, P->L.elems_u * P->esz, s));
+  CK(cudaMemsetAsync(vdt2, 0, P->L.elems_vdt2 * P->esz, s));
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
-  const uint64_t pb = P->L.pitch_x * 4, plb = pb * P->d.ny;
+  const uint64_t pb = P->L.pitch_x * P->esz, plb = pb * P->d.ny;
   for (int ki = 0; ki < KI_N; ++ki)
-    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, KCW(ki), KTY(ki)));
+    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, KCW(ki), KTY(ki), P->prec == 1));
   if (P->d.kernel == WAVE_KERNEL_TB2) {
     CKST(encode3d(&P->t2maps.v1, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, P->t2.tx + 2 * R, P->t2.ty + 2 * R));
     CKST(encode3d(&P->t2maps.v2, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, P->t2.tx, P->t2.ty));
   }
   for (int b = 0; b < 2; ++b) CKST(encode_buffer(P, b));
+  CKST(upload_maps(P));
   P->cur = 0;
   P->prv = 1;
   P->step = 0;
@@ -1018,24 +1121,34 @@ wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void
 static wave_status rebuild_inc(wave_plan* P, cudaStream_t s) {
   if (!P->src_set || !P->src_local || !P->have_vel) return WAVE_OK;
   const int64_t k = P->sk - P->d.z_offset;
-  const float* vsrc = P->vdt2 + (k * P->d.ny + P->sj) * P->L.pitch_x + P->si;
+  const float* vsrc = eo(P, P->vdt2, (k * P->d.ny + P->sj) * P->L.pitch_x + P->si);
   const int64_t ns = (int64_t)P->wavelet.size();
   P->ninc = ns;
   if (ns == 0) return WAVE_OK;
   CK(cudaMemcpyAsync(P->wl_d, P->wavelet.data(), ns * sizeof(float), cudaMemcpyHostToDevice, s));
-  k_inc<<<(unsigned)std::min<int64_t>((ns + 255) / 256, 1024), 256, 0, s>>>(P->inc_d, P->wl_d, ns, vsrc);
+  const unsigned nb = (unsigned)std::min<int64_t>((ns + 255) / 256, 1024);
+  if (P->prec)
+    k_inc<double><<<nb, 256, 0, s>>>(static_cast<double*>(P->inc_d), P->wl_d, ns,
+                                     reinterpret_cast<const double*>(vsrc));
+  else
+    k_inc<float><<<nb, 256, 0, s>>>(static_cast<float*>(P->inc_d), P->wl_d, ns, vsrc);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   return WAVE_OK;
 }
 
+// stats over a padded-pitch field of fp32 (f64 = false) or fp64 elements
 static wave_status field_stats(wave_plan* P, const float* base, int64_t rows, int positive, Stats* h,
-                               cudaStream_t s) {
+                               cudaStream_t s, bool f64 = false) {
   Stats init{0u, 0x7f7fffffu, 0u, 0u};
   CK(cudaMemcpyAsync(P->stats_d, &init, sizeof init, cudaMemcpyHostToDevice, s));
   const int64_t n = rows * P->d.nx;
   const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4 * 148 * 8));
-  k_stats<<<blocks, 256, 0, s>>>(base, P->L.pitch_x, (int)P->d.nx, rows, positive, P->stats_d);
+  if (f64)
+    k_stats<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(base), P->L.pitch_x, (int)P->d.nx, rows,
+                                           positive, P->stats_d);
+  else
+    k_stats<float><<<blocks, 256, 0, s>>>(base, P->L.pitch_x, (int)P->d.nx, rows, positive, P->stats_d);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(h, P->stats_d, sizeof(Stats), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -1048,10 +1161,18 @@ wave_status wave_set_velocity(wave_plan* P, const float* vel, int32_t where, voi
   if (!vel) return fail(WAVE_ERR_CONFIG, "vel is NULL");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t rows = P->d.ny * P->d.nz;
-  CK(cudaMemcpy2DAsync(P->vdt2, P->L.pitch_x * 4, vel, P->d.nx * 4, P->d.nx * 4, rows,
+  // V (fp32) goes into the vdt2 buffer itself (fp32 plans: converted in place)
+  // or into a stream-ordered temporary (fp64 plans)
+  float* vbuf = P->vdt2;
+  if (P->prec) CK(cudaMallocAsync(reinterpret_cast<void**>(&vbuf), P->L.elems_vdt2 * sizeof(float), s));
+  struct TmpFree {
+    float* p; cudaStream_t s;
+    ~TmpFree() { if (p) cudaFreeAsync(p, s); }
+  } tmp_free{P->prec ? vbuf : nullptr, s};
+  CK(cudaMemcpy2DAsync(vbuf, P->L.pitch_x * 4, vel, P->d.nx * 4, P->d.nx * 4, rows,
                        where == WAVE_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
   Stats st;
-  CKST(field_stats(P, P->vdt2, rows, 1, &st, s));
+  CKST(field_stats(P, vbuf, rows, 1, &st, s));
   P->have_vel = false;
   if (st.bad) return fail(WAVE_ERR_CONFIG, "velocity must be finite and > 0 (%u bad values)", st.bad);
   float vmax;
@@ -1061,7 +1182,11 @@ wave_status wave_set_velocity(wave_plan* P, const float* vel, int32_t where, voi
   const double cn = courant_number(P->d, vmax, dt);
   if (cn > 1.0) return fail(WAVE_ERR_CONFIG, "dt = %g violates the Courant limit (ratio %.4f > 1)", dt, cn);
   P->dt = dt;
-  k_vdt2<<<4 * 148, 256, 0, s>>>(P->vdt2, P->L.pitch_x, (int)P->d.nx, rows, (double)dt);
+  if (P->prec)
+    k_vdt2<double><<<4 * 148, 256, 0, s>>>(reinterpret_cast<double*>(P->vdt2), vbuf, P->L.pitch_x, (int)P->d.nx, rows,
+                                           (double)dt);
+  else
+    k_vdt2<float><<<4 * 148, 256, 0, s>>>(P->vdt2, vbuf, P->L.pitch_x, (int)P->d.nx, rows, (double)dt);
   CK(cudaGetLastError());
   CKST(refresh_tables(P, s));
   P->have_vel = true;
@@ -1083,7 +1208,7 @@ wave_status wave_set_source(wave_plan* P, int64_t i, int64_t j, int64_t k, const
   if (P->inc_d) { cudaFree(P->inc_d); P->inc_d = nullptr; }
   if (P->wl_d) { cudaFree(P->wl_d); P->wl_d = nullptr; }
   if (ns > 0) {
-    CK(cudaMalloc(&P->inc_d, ns * sizeof(float)));
+    CK(cudaMalloc(&P->inc_d, ns * P->esz));
     CK(cudaMalloc(&P->wl_d, ns * sizeof(float)));
   }
   P->si = i; P->sj = j; P->sk = k;
@@ -1102,10 +1227,10 @@ wave_status wave_set_state(wave_plan* P, const float* uprev, const float* ucur, 
   const float* src[4] = {ucur, uprev, nullptr, nullptr};
   for (int b = 0; b < 4; ++b) {
     if (!P->buf[b]) continue;
-    CK(cudaMemsetAsync(P->buf[b], 0, P->L.elems_u * sizeof(float), s));
+    CK(cudaMemsetAsync(P->buf[b], 0, P->L.elems_u * P->esz, s));
     if (src[b])
-      CK(cudaMemcpy2DAsync(P->buf[b] + R * P->L.pitch_x * P->d.ny, P->L.pitch_x * 4, src[b], P->d.nx * 4,
-                           P->d.nx * 4, P->d.ny * P->d.nz, kind, s));
+      CK(cudaMemcpy2DAsync(eo(P, P->buf[b], R * P->L.pitch_x * P->d.ny), P->L.pitch_x * P->esz, src[b],
+                           P->d.nx * P->esz, P->d.nx * P->esz, P->d.ny * P->d.nz, kind, s));
   }
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
   P->cur = 0;
@@ -1183,10 +1308,10 @@ wave_status wave_halo_views(const wave_plan* P, int32_t which, float** send_lo, 
   if (which != 0 && which != 1) return fail(WAVE_ERR_CONFIG, "which must be 0 or 1");
   const int64_t plane = P->L.pitch_x * P->d.ny, nz = P->d.nz;
   float* b = P->buf[which == 0 ? P->prv : P->cur];   // next (edges output) / current
-  if (send_lo) *send_lo = b + R * plane;
-  if (send_hi) *send_hi = b + nz * plane;
+  if (send_lo) *send_lo = eo(P, b, R * plane);
+  if (send_hi) *send_hi = eo(P, b, nz * plane);
   if (recv_lo) *recv_lo = b;
-  if (recv_hi) *recv_hi = b + (nz + R) * plane;
+  if (recv_hi) *recv_hi = eo(P, b, (nz + R) * plane);
   if (count) *count = R * plane;
   return WAVE_OK;
 }
@@ -1280,15 +1405,16 @@ wave_status wave_push_halo(wave_plan* P, int32_t which, void* stream) {
   if (which != 0 && which != 1) return fail(WAVE_ERR_CONFIG, "which must be 0 or 1");
   cudaStream_t s = (cudaStream_t)stream;
   const int bi = which == 1 ? P->cur : P->prv;
-  const int64_t plane = P->L.pitch_x * P->d.ny, nz = P->d.nz, n4 = R * plane / 4;
+  const int64_t plane = P->L.pitch_x * P->d.ny, nz = P->d.nz, n4 = R * plane * (int64_t)P->esz / 16;
   const unsigned blocks = (unsigned)std::min<int64_t>((n4 + 255) / 256, 4 * 148);
   if (P->peers.lo_buf[bi]) {
-    k_copy_planes<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(P->buf[bi] + R * plane),
-                                         reinterpret_cast<float4*>(P->peers.lo_buf[bi] + (P->peers.lo_nz + R) * plane), n4);
+    k_copy_planes<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(eo(P, P->buf[bi], R * plane)),
+                                         reinterpret_cast<float4*>(eo(P, P->peers.lo_buf[bi], (P->peers.lo_nz + R) * plane)),
+                                         n4);
     CK(cudaGetLastError());
   }
   if (P->peers.hi_buf[bi]) {
-    k_copy_planes<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(P->buf[bi] + nz * plane),
+    k_copy_planes<<<blocks, 256, 0, s>>>(reinterpret_cast<const float4*>(eo(P, P->buf[bi], nz * plane)),
                                          reinterpret_cast<float4*>(P->peers.hi_buf[bi]), n4);
     CK(cudaGetLastError());
   }
@@ -1299,8 +1425,8 @@ wave_status wave_read(const wave_plan* P, int32_t which, float* dst, int32_t whe
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
   if (!dst || (which != 0 && which != 1)) return fail(WAVE_ERR_CONFIG, "bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
-  const float* b = P->buf[which == 0 ? P->cur : P->prv] + R * P->L.pitch_x * P->d.ny;
-  CK(cudaMemcpy2DAsync(dst, P->d.nx * 4, b, P->L.pitch_x * 4, P->d.nx * 4, P->d.ny * P->d.nz,
+  const float* b = eo(P, P->buf[which == 0 ? P->cur : P->prv], R * P->L.pitch_x * P->d.ny);
+  CK(cudaMemcpy2DAsync(dst, P->d.nx * P->esz, b, P->L.pitch_x * P->esz, P->d.nx * P->esz, P->d.ny * P->d.nz,
                        where == WAVE_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
   if (where == WAVE_MEM_HOST) CK(cudaStreamSynchronize(s));
   return WAVE_OK;
@@ -1309,15 +1435,15 @@ wave_status wave_read(const wave_plan* P, int32_t which, float* dst, int32_t whe
 wave_status wave_field_ptr(const wave_plan* P, int32_t which, float** out) {
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
   if (!out || (which != 0 && which != 1)) return fail(WAVE_ERR_CONFIG, "bad arguments");
-  *out = P->buf[which == 0 ? P->cur : P->prv] + R * P->L.pitch_x * P->d.ny;
+  *out = eo(P, P->buf[which == 0 ? P->cur : P->prv], R * P->L.pitch_x * P->d.ny);
   return WAVE_OK;
 }
 
 wave_status wave_check_finite(wave_plan* P, float* h_maxabs, void* stream) {
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
   Stats st;
-  CKST(field_stats(P, P->buf[P->cur] + R * P->L.pitch_x * P->d.ny, P->d.ny * P->d.nz, 0, &st,
-                   (cudaStream_t)stream));
+  CKST(field_stats(P, eo(P, P->buf[P->cur], R * P->L.pitch_x * P->d.ny), P->d.ny * P->d.nz, 0, &st,
+                   (cudaStream_t)stream, P->prec == 1));
   float mx;
   memcpy(&mx, &st.max_bits, 4);
   if (h_maxabs) *h_maxabs = st.bad ? NAN : mx;
@@ -1392,7 +1518,8 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
       }
       if (src && source_in_frame(P, 8)) {
         CKST(mk(WAVE_KK_SOURCE, s));
-        k_source_at<<<1, 1, 0, s>>>(P->buf[c], source_offset(P), P->inc_d, P->ninc, P->dstep, 0);
+        k_source_at<<<1, 1, 0, s>>>(P->buf[c], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+                                    P->dstep, 0);
         CK(cudaEventRecord(recs.back().b, s));
       }
       for (const Launch& L : P->wall_p2) {
@@ -1402,7 +1529,8 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
       }
       if (src && source_in_frame(P, 4)) {
         CKST(mk(WAVE_KK_SOURCE, s));
-        k_source_at<<<1, 1, 0, s>>>(P->buf[d], source_offset(P), P->inc_d, P->ninc, P->dstep, 1);
+        k_source_at<<<1, 1, 0, s>>>(P->buf[d], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+                                    P->dstep, 1);
         CK(cudaEventRecord(recs.back().b, s));
       }
       CKST(mk(WAVE_KK_INTERIOR, s));
@@ -1484,6 +1612,7 @@ wave_status wave_plan_bind_aux(wave_plan* P, float* u2, float* u3, void* stream)
   CK(cudaMemsetAsync(u2, 0, P->L.elems_u * sizeof(float), s));
   CK(cudaMemsetAsync(u3, 0, P->L.elems_u * sizeof(float), s));
   for (int b = 2; b < 4; ++b) CKST(encode_buffer(P, b));
+  CKST(upload_maps(P));
   P->aux = true;
   drop_graphs(P);
   return WAVE_OK;

@@ -19,19 +19,19 @@ def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
     return int(s.cuda_stream)
 
 
-def _as_input(a, shape, device):
-    """Return (pointer, where, keepalive) for a dense fp32 array of `shape`."""
+def _as_input(a, shape, device, dtype=torch.float32):
+    """Return (pointer, where, keepalive) for a dense array of `shape` and `dtype`."""
     if isinstance(a, torch.Tensor):
         t = a.detach()
         if tuple(t.shape) != tuple(shape):
             raise ValueError(f"shape {tuple(t.shape)} != {tuple(shape)}")
-        t = t.to(dtype=torch.float32).contiguous()
+        t = t.to(dtype=dtype).contiguous()
         if t.is_cuda:
             if t.device != device:
                 t = t.to(device)
             return t.data_ptr(), _abi.WAVE_MEM_DEVICE, t
         return t.data_ptr(), _abi.WAVE_MEM_HOST, t
-    arr = np.ascontiguousarray(a, dtype=np.float32)
+    arr = np.ascontiguousarray(a, dtype=np.float64 if dtype == torch.float64 else np.float32)
     if arr.shape != tuple(shape):
         raise ValueError(f"shape {arr.shape} != {tuple(shape)}")
     return arr.ctypes.data, _abi.WAVE_MEM_HOST, arr
@@ -45,15 +45,19 @@ class WavePlan:
     eta_max      PML damping maximum (1/s);  kernel "stream" | "naive" | "tb2"
                  ("tb2": two-step temporal blocking, 4 wavefield buffers)
     nz_global, z_offset   slab position (defaults: single slab)
+    precision    "fp32" (default) or "fp64" (wavefields, vdt2 and arithmetic in
+                 double; the velocity and wavelet are still given in fp32)
     """
 
     def __init__(self, nx, ny, nz, w, h, dt, eta_max=4.0, kernel="stream",
-                 nz_global=None, z_offset=0, device=None, stream=None):
+                 nz_global=None, z_offset=0, device=None, stream=None, precision="fp32"):
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         kern = {"stream": _abi.WAVE_KERNEL_STREAM, "naive": _abi.WAVE_KERNEL_NAIVE,
                 "tb2": _abi.WAVE_KERNEL_TB2}[kernel]
+        prec = {"fp32": _abi.WAVE_PREC_FP32, "fp64": _abi.WAVE_PREC_FP64}[precision]
+        self.dtype = torch.float64 if prec == _abi.WAVE_PREC_FP64 else torch.float32
         self.desc = _abi.make_desc(nx, ny, nz, w, h, float(np.float32(dt)), eta_max, kern,
-                                   nz_global, z_offset)
+                                   nz_global, z_offset, prec)
         self.layout = _abi.wave_layout(self.desc)
         self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
         self.shape = (self.nz, self.ny, self.nx)
@@ -61,8 +65,8 @@ class WavePlan:
         with torch.cuda.device(self.device):
             L = self.layout
             nb = 4 if kern == _abi.WAVE_KERNEL_TB2 else 2
-            self.bufs = [torch.empty(L.elems_u, dtype=torch.float32, device=self.device) for _ in range(nb)]
-            self.vdt2 = torch.empty(L.elems_vdt2, dtype=torch.float32, device=self.device)
+            self.bufs = [torch.empty(L.elems_u, dtype=self.dtype, device=self.device) for _ in range(nb)]
+            self.vdt2 = torch.empty(L.elems_vdt2, dtype=self.dtype, device=self.device)
             self._plan = _abi.wave_plan_create(self.desc)
             _abi.wave_plan_bind(self._plan, self.bufs[0].data_ptr(), self.bufs[1].data_ptr(),
                                 self.vdt2.data_ptr(), _stream_handle(stream))
@@ -86,7 +90,7 @@ class WavePlan:
     def set_state(self, uprev=None, ucur=None, stream=None) -> None:
         """Initial u^{-1} / u^0 (None = zero); both host or both device arrays."""
         given = [a for a in (uprev, ucur) if a is not None]
-        conv = [_as_input(a, self.shape, self.device) for a in given]
+        conv = [_as_input(a, self.shape, self.device, self.dtype) for a in given]
         if len({c[1] for c in conv}) > 1:
             raise ValueError("uprev and ucur must both be host or both device arrays")
         where = conv[0][1] if conv else _abi.WAVE_MEM_HOST
@@ -146,8 +150,9 @@ class WavePlan:
         L = self.layout
         for b in self.bufs:
             off = ptr - b.data_ptr()
-            if 0 <= off < b.numel() * 4:
-                start = off // 4
+            es = b.element_size()
+            if 0 <= off < b.numel() * es:
+                start = off // es
                 v = b[start:start + self.nz * self.ny * L.pitch_x]
                 return v.view(self.nz, self.ny, L.pitch_x)[:, :, :self.nx]
         raise RuntimeError("field pointer outside the plan's buffers")
@@ -159,7 +164,9 @@ class WavePlan:
     def read(self, which: int = 0, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         """Dense copy of u^n / u^{n-1}; `out` may be a CUDA or (pinned) CPU tensor."""
         if out is None:
-            out = torch.empty(self.shape, dtype=torch.float32, device=self.device)
+            out = torch.empty(self.shape, dtype=self.dtype, device=self.device)
+        if out.dtype != self.dtype:
+            raise ValueError(f"out must be {self.dtype}")
         where = _abi.WAVE_MEM_DEVICE if out.is_cuda else _abi.WAVE_MEM_HOST
         with torch.cuda.device(self.device):
             _abi.wave_read(self._plan, which, out.data_ptr(), where, _stream_handle(stream))
@@ -173,8 +180,9 @@ class WavePlan:
         for p in (a, b, c, d):
             for buf in self.bufs:
                 off = p - buf.data_ptr()
-                if 0 <= off < buf.numel() * 4:
-                    out.append(buf[off // 4: off // 4 + n])
+                es = buf.element_size()
+                if 0 <= off < buf.numel() * es:
+                    out.append(buf[off // es: off // es + n])
                     break
         return tuple(out)
 

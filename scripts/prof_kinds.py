@@ -8,8 +8,9 @@ from paper_2009_04619_b200.wave import WavePlan
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 kernel = sys.argv[2] if len(sys.argv) > 2 else "stream"
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+prec = sys.argv[4] if len(sys.argv) > 4 else "fp32"
 s = synth.scenario(name)
-p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel)
+p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel, precision=prec)
 p.set_velocity(synth.velocity(s))
 p.set_source(*s.source, synth.wavelet_for(s, 4000))
 p.step(4)

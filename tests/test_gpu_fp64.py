@@ -1,0 +1,162 @@
+"""GPU parity of the fp64 path (WAVE_PREC_FP64, SPEC.md
+L82 verification precision) against the fp64 CPU oracle with unrounded fp64
+constants (oracle round32 = False).  Gate: max|Δ| / max|u_oracle| <= 1e-12
+(the two sides differ only by FMA contraction: ~1 ulp per operation, measured
+well below the gate); stream and naive fp64 kernels must agree bitwise."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _plan(s, kernel="stream", precision="fp64"):
+    from paper_2009_04619_b200.wave import WavePlan
+    return WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel, precision=precision)
+
+
+def run_gpu(s, steps, u0=None, um1=None, kernel="stream", precision="fp64"):
+    p = _plan(s, kernel, precision)
+    p.set_velocity(synth.velocity(s))
+    p.set_source(*s.source, synth.wavelet_for(s, max(steps, 1)))
+    if u0 is not None or um1 is not None:
+        p.set_state(um1, u0)
+    p.step(steps)
+    out = (p.read(0).cpu().numpy(), p.read(1).cpu().numpy())
+    p.close()
+    return out
+
+
+def run_oracle64(s, steps, u0=None, um1=None):
+    g = oracle.make_geom(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    u, up, st, _ = oracle.propagate(g, synth.velocity(s), synth.wavelet_for(s, max(steps, 1)), steps, s.source,
+                                    u0=u0, uprev0=um1, dtype=np.float64, round32=False)
+    assert st == 0
+    return u, up
+
+
+def rel_linf(got, ref):
+    m = float(np.abs(ref).max())
+    return float(np.abs(got - ref).max()) / (m if m > 0 else 1.0)
+
+
+def test_fp64_point_source_c1():
+    s = synth.scenario("C1")
+    g, gp = run_gpu(s, s.steps)
+    assert g.dtype == np.float64
+    r, rp = run_oracle64(s, s.steps)
+    assert rel_linf(g, r) <= TOL64 and rel_linf(gp, rp) <= TOL64, (rel_linf(g, r), rel_linf(gp, rp))
+
+
+@pytest.mark.parametrize("name,kw,steps", [
+    ("C1", {}, 30),
+    ("RAGGED", {}, 25),
+    ("RAGGED", dict(w=0), 9),
+    ("RAGGED", dict(nx=9, ny=11, nz=10, w=2, src=(4, 5, 5)), 7),
+    ("RAGGED", dict(w=20, nx=70, ny=45, nz=53, src=(35, 22, 26)), 7),
+    ("C1", dict(h=(10.0, 7.5, 12.5), eta_max=30.0), 12),
+    ("RAGGED", dict(nx=203, ny=150, nz=40, w=16, src=(101, 75, 20)), 6),
+])
+def test_fp64_random_state(name, kw, steps):
+    s = synth.scenario(name, **kw)
+    sh = (s.nz, s.ny, s.nx)
+    u0 = synth.random_state(sh, 51).astype(np.float64)
+    um1 = synth.random_state(sh, 52).astype(np.float64)
+    g, _ = run_gpu(s, steps, u0, um1)
+    r, _ = run_oracle64(s, steps, u0, um1)
+    assert rel_linf(g, r) <= TOL64, rel_linf(g, r)
+
+
+@pytest.mark.parametrize("name", ["C1", "RAGGED"])
+def test_fp64_stream_equals_naive_bitwise(name):
+    s = synth.scenario(name)
+    sh = (s.nz, s.ny, s.nx)
+    u0 = synth.random_state(sh, 61).astype(np.float64)
+    a, ap = run_gpu(s, 14, u0, None, kernel="stream")
+    b, bp = run_gpu(s, 14, u0, None, kernel="naive")
+    assert np.array_equal(a, b) and np.array_equal(ap, bp)
+
+
+def test_fp64_differs_from_fp32_by_fp32_rounding_only():
+    # same scheme in two precisions: O(1e-6) apart after a few steps, never more
+    s = synth.scenario("C1")
+    sh = (s.nz, s.ny, s.nx)
+    u0 = synth.random_state(sh, 71)
+    g64, _ = run_gpu(s, 10, u0.astype(np.float64))
+    g32, _ = run_gpu(s, 10, u0, precision="fp32")
+    d = rel_linf(g32.astype(np.float64), g64)
+    assert 0 < d < 1e-5, d
+
+
+def test_fp64_source_first_step_exact():
+    # from the zero state one step leaves exactly (V dt)^2 w[0] (fp64) at the source
+    s = synth.scenario("RAGGED")
+    wl = np.array([0.75], np.float32)
+    p = _plan(s)
+    V = synth.velocity(s)
+    p.set_velocity(V)
+    p.set_source(*s.source, wl)
+    p.step(1)
+    u = p.read(0).cpu().numpy()
+    i, j, k = s.source
+    vdt = float(V[k, j, i]) * float(np.float32(s.dt))
+    assert u[k, j, i] == vdt * vdt * 0.75
+    u[k, j, i] = 0
+    assert not u.any()
+    p.close()
+
+
+def test_fp64_tb2_rejected():
+    from paper_2009_04619_b200._abi import WaveError
+    s = synth.scenario("C1")
+    with pytest.raises(WaveError):
+        _plan(s, kernel="tb2")
+
+
+def test_fp64_full_size_c2_sampled():
+    # BASELINE.json configs[1] (512^3) in fp64 through the production kernels:
+    # 4 steps from a random state, compared on a z-slab of the oracle (the
+    # slab's 4-plane halos of the full-grid state make it exact for 1 step per
+    # halo plane; 4 steps need 16 extra planes each side)
+    s = synth.scenario("C2")
+    steps, z0, z1 = 4, 250, 262
+    sh = (s.nz, s.ny, s.nx)
+    rng = np.random.Generator(np.random.PCG64(81))
+    u0 = rng.uniform(-1, 1, size=sh)
+    p = _plan(s)
+    p.set_velocity(synth.velocity(s))
+    p.set_source(*s.source, synth.wavelet_for(s, steps))
+    p.set_state(None, u0)
+    p.step(steps)
+    got = p.read(0)[z0:z1].cpu().numpy()
+    p.close()
+    a, b = z0 - 4 * steps, z1 + 4 * steps
+    g = oracle.make_geom(s.nx, s.ny, b - a, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=a)
+    V = synth.velocity(s)[a:b]
+    vd = oracle.vdt2(V, s.dt, round32=False, dtype=np.float64)
+    uu = oracle.pad(u0[a - 4:b + 4][4:-4], np.float64)
+    uu[:4, 4:-4, 4:-4] = u0[a - 4:a]
+    uu[-4:, 4:-4, 4:-4] = u0[b:b + 4]
+    up = np.zeros_like(uu)
+    wl = synth.wavelet_for(s, steps)
+    for n in range(steps):
+        assert oracle.step_padded(g, uu, up, vd, s.source, float(wl[n]), round32=False) == 0
+        uu, up = up, uu
+        # the slab's own z halos are stale after a step; the sampled planes stay
+        # exact because they are >= 4*(steps-n) planes from the slab ends
+    ref = uu[4 + z0 - a:4 + z1 - a, 4:-4, 4:-4]
+    assert rel_linf(got, ref) <= TOL64

@@ -372,7 +372,8 @@ for name in ("RAGGED", "C1"):
 @pytest.mark.parametrize("env", [
     {"WAVE25_INNER_TILE": "128x16x1"}, {"WAVE25_INNER_TILE": "64x16x1"},
     {"WAVE25_INNER_TILE": "128x8x1"}, {"WAVE25_INNER_TILE": "248x8x1"}, {"WAVE25_INNER_TILE": "224x8x1"},
-    {"WAVE25_INNER_TILE": "248x8x2"},
+    {"WAVE25_INNER_TILE": "248x8x2"}, {"WAVE25_INNER_TILE": "256x8x1r"},
+    {"WAVE25_FUSED": "1", "WAVE25_FUSED_TILE": "fused128x8x1"},
     {"WAVE25_ABLATION": "gmem_32x4x1"}, {"WAVE25_ABLATION": "gmem_8x8x8"}, {"WAVE25_ABLATION": "smem_u"},
     {"WAVE25_ABLATION": "st_smem_32x16"}, {"WAVE25_ABLATION": "st_reg_shft_32x16"},
     {"WAVE25_ABLATION": "st_reg_fixed_32x16"}, {"WAVE25_ABLATION": "st_reg_fixed_32x32"},
@@ -490,3 +491,43 @@ def test_peer_slab_runner_two_processes_bitwise():
     ref, _ = run_gpu(s, steps, synth.random_state(sh, 61), synth.random_state(sh, 62),
                      wl=synth.wavelet_for(s, steps))
     assert np.array_equal(got, ref)
+
+
+RACE_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, sys.argv[1])
+import synth
+from paper_2009_04619_b200.wave import WavePlan
+s = synth.scenario("RAGGED")
+sh = (s.nz, s.ny, s.nx)
+for t in range(int(sys.argv[2])):
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    p.set_velocity(synth.velocity(s))
+    p.set_source(*s.source, synth.wavelet_for(s, 12))
+    p.set_state(synth.random_state(sh, 41), synth.random_state(sh, 42))
+    for n in range(12):
+        p.step(1)
+    print(hashlib.sha256(p.read(0).cpu().numpy().tobytes()).hexdigest())
+    p.close()
+"""
+
+
+def test_concurrent_walls_repeatable():
+    # Regression test for a cross-proxy WAR hazard: consumer warps read a ring
+    # stage with generic loads, release it, and the producer's TMA (async
+    # proxy) refilled it -- without fence.proxy.async the overwrite could land
+    # before slow loads completed.  It showed (~4 % of runs) when the x-wall
+    # kernel shared SMs with many short interior blocks (the gmem ablation
+    # shape) and steps were enqueued back to back.  30 such runs must all equal
+    # the serial (one-stream) reference.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("WAVE25_")}
+    ref = subprocess.run([sys.executable, "-c", RACE_SCRIPT, root, "1"], env={**base, "WAVE25_SERIAL": "1"},
+                         capture_output=True, text=True, check=True).stdout.split()
+    got = subprocess.run([sys.executable, "-c", RACE_SCRIPT, root, "30"],
+                         env={**base, "WAVE25_ABLATION": "gmem_8x8x8"}, capture_output=True, text=True,
+                         check=True).stdout.split()
+    assert len(got) == 30 and set(got) == set(ref), (len(set(got)), got.count(ref[0]))
