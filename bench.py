@@ -60,7 +60,7 @@ def workload(config: str, world: int):
     s = synth.scenario(config)
     if config == "C3":
         desc = ("C3: 1024^3 extended grid (992^3 inner + 16-cell PML on every face), layered V "
-                "1500->4500 m/s in 8 z-layers, Ricker 15 Hz at the centre, fp32 (BASELINE.json configs[2])")
+                "1500->4500 m/s in 8 z-layers, Ricker 15 Hz at the centre (BASELINE.json configs[2])")
     elif config == "C2":
         desc = "C2: 512^3 extended grid, 16-cell PML, constant V 2000 m/s, Ricker 20 Hz, fp32 (configs[1])"
     else:
@@ -288,7 +288,10 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    plan = WavePlan(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
+    kern = args.kernel if world == 1 else "stream"
+    plan = WavePlan(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off, kernel=kern,
+                    precision=args.precision)
+    bpp = BYTES_PER_POINT * (2 if args.precision == "fp64" else 1)   # algorithmic bytes per point-step
     plan.set_velocity(V)
     plan.set_source(*s.source, wl)
     halo = os.environ.get("WAVE25_HALO", "peer")     # peer: fused peer stores; nccl: send/recv
@@ -329,21 +332,24 @@ def run_ours(args, rank, world, local):
         ms, clocks = timed()
         remeasured = True
     value = pts_total * args.steps / (ms / 1e3) / 1e9
-    launches = plan.launches_per_step * args.steps
+    launches = plan.launches(args.steps) if world == 1 else plan.launches_per_step * args.steps
 
     # ---- roofline of the dominant (interior) kernel: profiled pass -------
     roof = None
     kpts = plan.kernel_points()
     if world == 1 and not args.no_profile:
-        kms, kn = plan.step_profiled(args.steps, stream=stream)
+        kms, kn = plan.step_profiled(args.steps - args.steps % plan.steps_per_launch, stream=stream)
         t_launch = kms["interior"] / max(kn["interior"], 1)            # ms per launch
-        achieved = BYTES_PER_POINT * kpts["interior"] / (t_launch / 1e3) / 1e9
+        # a two-step (TB2) launch reads u^n, u^{n-1}, vdt2 once and writes two levels: 20 B per point
+        bpl = 20 if plan.steps_per_launch == 2 else bpp                  # algorithmic bytes per point per launch
+        achieved = bpl * kpts["interior"] / (t_launch / 1e3) / 1e9
         peak, peak_src = measured_peak()
         step_ms_prof = sum(kms.values()) / max(args.steps, 1)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic("interior"),
-                "kernel": "k_stream interior (TMA z-streaming, 25-pt)",
-                "points_per_launch": kpts["interior"], "bytes_per_point": BYTES_PER_POINT,
+                "traffic": ncu_traffic("interior") if (args.precision == "fp32" and args.kernel == "stream") else None,
+                "kernel": ("k_tb2 interior (two-step temporal blocking)" if plan.steps_per_launch == 2
+                           else "k_stream interior (TMA z-streaming, 25-pt)"),
+                "points_per_launch": kpts["interior"], "bytes_per_point": bpl,
                 "ms_per_launch": t_launch, "peak_source": peak_src,
                 "kernel_ms_per_step": {k: v / max(args.steps, 1) for k, v in kms.items()},
                 "kernel_points_per_step": kpts,
@@ -358,7 +364,7 @@ def run_ours(args, rank, world, local):
     e2e = None
     if not args.no_e2e:
         Vh = torch.from_numpy(V).pin_memory()
-        outh = torch.empty((nzl, s.ny, s.nx), dtype=torch.float32).pin_memory()
+        outh = torch.empty((nzl, s.ny, s.nx), dtype=plan.dtype).pin_memory()
         barrier()
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -374,7 +380,7 @@ def run_ours(args, rank, world, local):
         e_ms = maxall(max(e0.elapsed_time(e1), 1e3 * wall))
         h2d = V.nbytes + 4 * len(wl)
         e2e = {"value": pts_total * args.steps / (e_ms / 1e3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": outh.numel() * 4 / args.steps,
+               "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": outh.numel() * outh.element_size() / args.steps,
                "ms_total": e_ms, "api": "WavePlan.set_state/set_velocity(host)/set_source/step/read(host) "
                                          "-> libwave25.so C ABI"}
 
@@ -386,17 +392,19 @@ def run_ours(args, rank, world, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "data": "synthetic",
             "config": {"workload": desc, "grid": [s.nx, s.ny, s.nz], "points_per_step": pts_total,
                        "pml_width": s.w, "parallelism": f"z-slab x{world}" if world > 1 else "1 GPU",
-                       "l2": f"no flush: {BYTES_PER_POINT * pts_total / 1e9:.1f} GB streamed per step >> 126 MB L2",
+                       "l2": f"no flush: {bpp * pts_total / 1e9:.1f} GB streamed per step >> 126 MB L2",
+                       "precision": args.precision, "kernel_family": kern,
                        "kernels": "interior + x-walls + y-walls (2 streams, joined) + source, CUDA graph"
                                   if world == 1 else (
                                       "fused halo: stencil kernels store edge planes into the neighbours' ghost "
                                       "planes over NVLink (IPC peer mapping) + device step flags, CUDA graph"
                                       if halo == "peer" else "edges -> NCCL send/recv || interior, joined")},
-            "hbm_gbs_at_16B": value * BYTES_PER_POINT,
-            "frac_of_measured_hbm": value * BYTES_PER_POINT / measured_peak()[0],
+            "hbm_gbs_at_algorithmic_bytes": value * bpp,
+            "frac_of_measured_hbm": value * bpp / measured_peak()[0],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks, "remeasured": remeasured,
         }
@@ -417,6 +425,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--kernel", choices=["stream", "tb2"], default="stream",
+                    help="1 GPU: stream (default) or tb2 two-step temporal blocking")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = env_rank()
