@@ -76,6 +76,10 @@ def lib():
                 f.argtypes = [ctypes.POINTER(Geom), i32, P, P, i64, i64, i64, i64, P, P, i64,
                               ctypes.POINTER(i64)]
                 f.restype = i32
+                f = getattr(L, f"oracle_propagate_eta_{sfx}")
+                f.argtypes = [ctypes.POINTER(Geom), i32, P, P, P, i64, i64, i64, i64, P, P, i64,
+                              ctypes.POINTER(i64)]
+                f.restype = i32
                 f = getattr(L, f"oracle_constants_{sfx}")
                 f.argtypes = [ctypes.POINTER(Geom), i32, P, P, P, P, P]
                 f.restype = i32
@@ -136,11 +140,14 @@ def dt_auto(h, V: np.ndarray) -> np.float32:
 
 def propagate(g: Geom, V: np.ndarray, wavelet: np.ndarray, T: int, src,
               u0: Optional[np.ndarray] = None, uprev0: Optional[np.ndarray] = None,
-              dtype=np.float32, round32: bool = True, check_every: int = 0):
+              dtype=np.float32, round32: bool = True, check_every: int = 0,
+              eta: Optional[np.ndarray] = None):
     """Algorithm 1 for T steps on a full (single-slab) grid.
 
     Returns (u^T, u^{T-1}, status, fail_step) as dense [nz][ny][nx] arrays of
     `dtype`.  Inputs u0 = u^0 and uprev0 = u^{-1} default to zero.
+    eta: None (the eta_max (d/w)^2 profile) or a user-supplied fp32 eta field
+    [nz][ny][nx] (stored-eta variant, R16).
     """
     dt_ = np.dtype(dtype)
     shape = (g.nz, g.ny, g.nx)
@@ -153,9 +160,12 @@ def propagate(g: Geom, V: np.ndarray, wavelet: np.ndarray, T: int, src,
         wl = np.concatenate([wl, np.zeros(T - wl.size, np.float32)])
     fail = ctypes.c_int64(-1)
     si, sj, sk = (int(v) for v in src)
-    st = getattr(lib(), f"oracle_propagate_{_sfx(dt_)}")(
-        ctypes.byref(g), int(round32), _ptr(V), _ptr(wl), int(T), si, sj, sk,
-        _ptr(u), _ptr(up), int(check_every), ctypes.byref(fail))
+    if eta is not None:
+        eta = np.ascontiguousarray(eta, dtype=np.float32)
+        assert eta.shape == shape, (eta.shape, shape)
+    st = getattr(lib(), f"oracle_propagate_eta_{_sfx(dt_)}")(
+        ctypes.byref(g), int(round32), _ptr(V), None if eta is None else _ptr(eta), _ptr(wl), int(T),
+        si, sj, sk, _ptr(u), _ptr(up), int(check_every), ctypes.byref(fail))
     return u, up, int(st), int(fail.value)
 
 

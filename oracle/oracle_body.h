@@ -17,8 +17,11 @@
  * up_pad  : u^{n-1} on entry, u^{n+1} on exit (same layout).
  * vdt2    : dense [nz][ny][nx] fp (V*dt)^2 values.
  */
+static REAL SFX(eta_star)(const oracle_geom *g, const struct SFX(consts) *K, const REAL *eta_arr,
+                          int64_t i, int64_t j, int64_t kg);
+
 static void SFX(sweep)(const oracle_geom *g, const struct SFX(consts) *K,
-                       const REAL *u, REAL *up, const REAL *vdt2)
+                       const REAL *u, REAL *up, const REAL *vdt2, const REAL *eta_arr)
 {
     const int64_t nx = g->nx, ny = g->ny, nz = g->nz;
     const int64_t sy = nx + 2 * R, sz = (ny + 2 * R) * sy;
@@ -50,18 +53,37 @@ static void SFX(sweep)(const oracle_geom *g, const struct SFX(consts) *K,
                      *          / (1 + eta dt),  d_a f = (f(+1) - f(-1)) / (2 h_a).
                      * eta is read on the 7-point star. */
                     REAL gsum = 0;
-                    gsum = gsum + ((SFX(eta_at)(g, K, i + 1, j, kg) - SFX(eta_at)(g, K, i - 1, j, kg)) * K->i2h[0])
+                    gsum = gsum + ((SFX(eta_star)(g, K, eta_arr, i + 1, j, kg) - SFX(eta_star)(g, K, eta_arr, i - 1, j, kg)) * K->i2h[0])
                                 * ((u[p + 1] - u[p - 1]) * K->i2h[0]);
-                    gsum = gsum + ((SFX(eta_at)(g, K, i, j + 1, kg) - SFX(eta_at)(g, K, i, j - 1, kg)) * K->i2h[1])
+                    gsum = gsum + ((SFX(eta_star)(g, K, eta_arr, i, j + 1, kg) - SFX(eta_star)(g, K, eta_arr, i, j - 1, kg)) * K->i2h[1])
                                 * ((u[p + sy] - u[p - sy]) * K->i2h[1]);
-                    gsum = gsum + ((SFX(eta_at)(g, K, i, j, kg + 1) - SFX(eta_at)(g, K, i, j, kg - 1)) * K->i2h[2])
+                    gsum = gsum + ((SFX(eta_star)(g, K, eta_arr, i, j, kg + 1) - SFX(eta_star)(g, K, eta_arr, i, j, kg - 1)) * K->i2h[2])
                                 * ((u[p + sz] - u[p - sz]) * K->i2h[2]);
-                    un = (((REAL)2 * uc - K->A[d] * up[p]) + vdt2[q] * (L + gsum)) / K->B[d];
+                    REAL A = K->A[d], B = K->B[d];
+                    if (eta_arr) {
+                        /* stored eta (R16): A = 1 - eta dt, B = 1 + eta dt from
+                         * this point's stored value, computed in fp64, rounded once */
+                        const double e = (double)eta_arr[q], dt = (double)g->dt;
+                        A = (REAL)(K->round32 ? fp32_round(1.0 - e * dt) : 1.0 - e * dt);
+                        B = (REAL)(K->round32 ? fp32_round(1.0 + e * dt) : 1.0 + e * dt);
+                    }
+                    un = (((REAL)2 * uc - A * up[p]) + vdt2[q] * (L + gsum)) / B;
                 }
                 up[p] = un;
             }
         }
     }
+}
+
+/* eta on the 7-point star: the stored field (user-supplied eta, SURVEY.md
+ * §8(f) rank 3; dense [nz][ny][nx] of this single-slab grid) or the profile
+ * eta_{d(q)}; 0 outside the domain either way. */
+static REAL SFX(eta_star)(const oracle_geom *g, const struct SFX(consts) *K, const REAL *eta_arr,
+                          int64_t i, int64_t j, int64_t kg)
+{
+    if (!eta_arr) return SFX(eta_at)(g, K, i, j, kg);
+    if (!inside(g, i, j, kg)) return 0;
+    return eta_arr[((kg - g->z_offset) * g->ny + j) * g->nx + i];
 }
 
 /* Source injection, PAPER.md L263 (Alg. 1 "u^n = u^n + f^n") with the Eq. 2
@@ -99,7 +121,7 @@ EXPORT int SFX(oracle_step)(const oracle_geom *g, int round32, const REAL *u_pad
 {
     struct SFX(consts) K;
     if (SFX(make_consts)(g, round32, &K)) return ORACLE_ERR_CONFIG;
-    SFX(sweep)(g, &K, u_pad, up_pad, vdt2);
+    SFX(sweep)(g, &K, u_pad, up_pad, vdt2, NULL);
     SFX(inject)(g, up_pad, vdt2, si, sj, sk, wn, round32);
     SFX(free_consts)(&K);
     return ORACLE_OK;
@@ -110,20 +132,31 @@ EXPORT int SFX(oracle_step)(const oracle_geom *g, int round32, const REAL *u_pad
  * u^0, u^{-1} ("u^0 := 0" is the all-zero input); out: u^T,
  * u^{T-1}.  Non-finite check every `check_every` steps (0 = only at the end):
  * returns ORACLE_ERR_UNSTABLE and the step count in *fail_step. */
-EXPORT int SFX(oracle_propagate)(const oracle_geom *g, int round32, const float *V,
-                                 const float *wavelet, int64_t T, int64_t si, int64_t sj,
-                                 int64_t sk, REAL *u, REAL *up, int64_t check_every,
-                                 int64_t *fail_step)
+/* eta_in: NULL (the eta_max (d/w)^2 profile) or a user-supplied eta field,
+ * dense [nz][ny][nx] fp32, >= 0 (stored-eta variant, R16). */
+EXPORT int SFX(oracle_propagate_eta)(const oracle_geom *g, int round32, const float *V,
+                                     const float *eta_in, const float *wavelet, int64_t T, int64_t si,
+                                     int64_t sj, int64_t sk, REAL *u, REAL *up, int64_t check_every,
+                                     int64_t *fail_step)
 {
     struct SFX(consts) K;
     if (g->z_offset != 0 || g->nz_global != g->nz) return ORACLE_ERR_CONFIG;
     if (SFX(make_consts)(g, round32, &K)) return ORACLE_ERR_CONFIG;
     const int64_t n = g->nx * g->ny * g->nz;
+    REAL *eta_arr = NULL;
+    if (eta_in) {
+        eta_arr = (REAL *)malloc(sizeof(REAL) * n);
+        if (!eta_arr) { SFX(free_consts)(&K); return ORACLE_ERR_ALLOC; }
+        for (int64_t q = 0; q < n; ++q) eta_arr[q] = (REAL)eta_in[q];
+    }
     const int64_t np = (g->nx + 2 * R) * (g->ny + 2 * R) * (g->nz + 2 * R);
     REAL *vdt2 = (REAL *)malloc(sizeof(REAL) * n);
     REAL *a = (REAL *)calloc(np, sizeof(REAL));
     REAL *b = (REAL *)calloc(np, sizeof(REAL));
-    if (!vdt2 || !a || !b) { free(vdt2); free(a); free(b); SFX(free_consts)(&K); return ORACLE_ERR_ALLOC; }
+    if (!vdt2 || !a || !b) {
+        free(vdt2); free(a); free(b); free(eta_arr); SFX(free_consts)(&K);
+        return ORACLE_ERR_ALLOC;
+    }
     SFX(vdt2_fill)(V, n, g->dt, round32, vdt2);
     for (int64_t k = 0; k < g->nz; ++k)
         for (int64_t j = 0; j < g->ny; ++j)
@@ -135,7 +168,7 @@ EXPORT int SFX(oracle_propagate)(const oracle_geom *g, int round32, const float 
     int status = ORACLE_OK;
     if (fail_step) *fail_step = -1;
     for (int64_t s = 0; s < T; ++s) {
-        SFX(sweep)(g, &K, cur, prev, vdt2);                     /* prev <- u^{s+1} */
+        SFX(sweep)(g, &K, cur, prev, vdt2, eta_arr);            /* prev <- u^{s+1} */
         SFX(inject)(g, prev, vdt2, si, sj, sk, wavelet[s], round32); /* + f^{s+1}   */
         REAL *t = cur; cur = prev; prev = t;                    /* role swap        */
         if ((check_every > 0 && (s + 1) % check_every == 0) || s + 1 == T) {
@@ -152,9 +185,18 @@ EXPORT int SFX(oracle_propagate)(const oracle_geom *g, int round32, const float 
                 u[(k * g->ny + j) * g->nx + i] = cur[pidx(g, i, j, k)];
                 up[(k * g->ny + j) * g->nx + i] = prev[pidx(g, i, j, k)];
             }
-    free(vdt2); free(a); free(b);
+    free(vdt2); free(a); free(b); free(eta_arr);
     SFX(free_consts)(&K);
     return status;
+}
+
+EXPORT int SFX(oracle_propagate)(const oracle_geom *g, int round32, const float *V,
+                                 const float *wavelet, int64_t T, int64_t si, int64_t sj,
+                                 int64_t sk, REAL *u, REAL *up, int64_t check_every,
+                                 int64_t *fail_step)
+{
+    return SFX(oracle_propagate_eta)(g, round32, V, NULL, wavelet, T, si, sj, sk, u, up, check_every,
+                                     fail_step);
 }
 
 /* The fp constants the oracle uses (for the pins in tests/): c[13] =

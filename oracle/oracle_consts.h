@@ -13,6 +13,7 @@ static int SFX(make_consts)(const oracle_geom *g, int round32, struct SFX(consts
     if (g->nx < 1 || g->ny < 1 || g->nz < 1 || g->w < 0) return 1;
     if (!(g->hx > 0 && g->hy > 0 && g->hz > 0)) return 1;
     double (*rnd)(double) = round32 ? fp32_round : NULL;
+    K->round32 = round32;
 #define RND(x) (rnd ? rnd(x) : (x))
     const double ih2[3] = { 1.0 / (g->hx * g->hx), 1.0 / (g->hy * g->hy), 1.0 / (g->hz * g->hz) };
     /* c_xyz = w0 (1/hx^2 + 1/hy^2 + 1/hz^2)  (SPEC.md L125 with per-axis h, R1) */

@@ -88,7 +88,7 @@ static double fp32_round(double x) { return (double)(float)x; }
 /* ---------------- instantiate for float ---------------- */
 #define REAL float
 #define SFX(name) name##_f32
-struct consts_f32 { float c0, cx[R + 1], cy[R + 1], cz[R + 1], i2h[3]; float *eta, *A, *B; };
+struct consts_f32 { float c0, cx[R + 1], cy[R + 1], cz[R + 1], i2h[3]; float *eta, *A, *B; int round32; };
 #include "oracle_consts.h"
 #include "oracle_body.h"
 #undef REAL
@@ -97,7 +97,7 @@ struct consts_f32 { float c0, cx[R + 1], cy[R + 1], cz[R + 1], i2h[3]; float *et
 /* ---------------- instantiate for double ---------------- */
 #define REAL double
 #define SFX(name) name##_f64
-struct consts_f64 { double c0, cx[R + 1], cy[R + 1], cz[R + 1], i2h[3]; double *eta, *A, *B; };
+struct consts_f64 { double c0, cx[R + 1], cy[R + 1], cz[R + 1], i2h[3]; double *eta, *A, *B; int round32; };
 #include "oracle_consts.h"
 #include "oracle_body.h"
 #undef REAL

@@ -515,3 +515,105 @@ def test_source_location_and_scaling_asymmetric(oracle_lib):
     assert u[k, j, i] == pytest.approx(exp, rel=1e-15)
     u[k, j, i] = 0
     assert not u.any()
+
+
+# --------------------------------------------------------------------------
+# Stored (user-supplied) eta -- SURVEY.md §8(f) rank 3, R16
+# --------------------------------------------------------------------------
+
+def _random_eta(shape, seed, scale=20.0):
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return (scale * rng.random(shape)).astype(np.float32)
+
+
+def test_stored_eta_dense_operator_brute_force(oracle_lib):
+    # Same independent Kronecker formulation as above, with an arbitrary
+    # (random, non-smooth) stored eta field: grad eta from the stored values
+    # with 0 outside the domain, A = 1 - eta dt and B = 1 + eta dt per PML point.
+    # A transposed eta index or a wrong neighbour fails at O(1).
+    nx, ny, nz, w = 9, 10, 11, 2
+    hx, hy, hz = 10.0, 8.0, 12.0
+    dt = float(np.float32(1e-3))
+    g = geom(nx, ny, nz, w=w, h=(hx, hy, hz), dt=dt, eta_max=7.0)   # eta_max unused by stored eta
+    wf = [float(x) for x in W]
+
+    def d2(n, h):
+        M = np.zeros((n, n))
+        for i in range(n):
+            M[i, i] = wf[0] / h ** 2
+            for m in range(1, 5):
+                for j in (i - m, i + m):
+                    if 0 <= j < n:
+                        M[i, j] = wf[m] / h ** 2
+        return M
+
+    def d1(n, h):
+        return (np.eye(n, k=1) - np.eye(n, k=-1)) / (2 * h)
+
+    Ix, Iy, Iz = np.eye(nx), np.eye(ny), np.eye(nz)
+    kron3 = lambda A, B, C: np.kron(A, np.kron(B, C))
+    Lap = kron3(Iz, Iy, d2(nx, hx)) + kron3(Iz, d2(ny, hy), Ix) + kron3(d2(nz, hz), Iy, Ix)
+    G = [kron3(Iz, Iy, d1(nx, hx)), kron3(Iz, d1(ny, hy), Ix), kron3(d1(nz, hz), Iy, Ix)]
+    eta32 = _random_eta((nz, ny, nx), 9)
+    eta = eta32.astype(np.float64).ravel()
+    ge = [Gk @ eta for Gk in G]                        # central differences, eta = 0 outside
+    _, d = _eta_field(nx, ny, nz, w, 1.0)
+    pml = d.ravel() > 0
+    V = synth.velocity(synth.scenario("RAGGED", nx=nx, ny=ny, nz=nz, seed=8))
+    D = ((V.astype(np.float64) * dt) ** 2).ravel()
+    Op = Lap + pml[:, None] * (ge[0][:, None] * G[0] + ge[1][:, None] * G[1] + ge[2][:, None] * G[2])
+    Acoef = np.where(pml, 1 - eta * dt, 1.0)
+    Bcoef = np.where(pml, 1 + eta * dt, 1.0)
+    u = synth.random_state((nz, ny, nx), 23).astype(np.float64).ravel()
+    up = synth.random_state((nz, ny, nx), 24).astype(np.float64).ravel()
+    u0, up0 = u.copy(), up.copy()
+    for _ in range(3):
+        un = (2 * u - Acoef * up + D * (Op @ u)) / Bcoef
+        u, up = un, u
+    got, gotp, st, _ = oracle.propagate(g, V, np.zeros(3, np.float32), 3, (4, 5, 5),
+                                        u0=u0.reshape(nz, ny, nx), uprev0=up0.reshape(nz, ny, nx),
+                                        dtype=np.float64, round32=False, eta=eta32)
+    assert st == 0
+    np.testing.assert_allclose(got.ravel(), u, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(gotp.ravel(), up, rtol=0, atol=1e-12)
+
+
+def test_stored_eta_linear_ramp_probe(oracle_lib):
+    # closed form of the ramp probe with an arbitrary stored eta field
+    nx, ny, nz, w = 27, 25, 23, 6
+    hx, hy, hz = 10.0, 7.5, 12.5
+    dt = float(np.float32(1.5e-3))
+    g = geom(nx, ny, nz, w=w, h=(hx, hy, hz), dt=dt, eta_max=0.0)
+    C, a, b, c = 0.7, 0.37, -0.21, 0.29
+    X = np.arange(nx)[None, None, :] * hx
+    Y = np.arange(ny)[None, :, None] * hy
+    Z = np.arange(nz)[:, None, None] * hz
+    u = C + a * X + b * Y + c * Z + np.zeros((nz, ny, nx))
+    V = synth.velocity(synth.scenario("RAGGED", nx=nx, ny=ny, nz=nz, seed=3))
+    eta32 = _random_eta((nz, ny, nx), 10, scale=40.0)
+    out, _, st, _ = oracle.propagate(g, V, np.zeros(1, np.float32), 1, (nx // 2, ny // 2, nz // 2), u0=u,
+                                     uprev0=u.copy(), dtype=np.float64, round32=False, eta=eta32)
+    assert st == 0
+    ep = np.pad(eta32.astype(np.float64), 1)
+    gx = (ep[1:-1, 1:-1, 2:] - ep[1:-1, 1:-1, :-2]) / (2 * hx)
+    gy = (ep[1:-1, 2:, 1:-1] - ep[1:-1, :-2, 1:-1]) / (2 * hy)
+    gz = (ep[2:, 1:-1, 1:-1] - ep[:-2, 1:-1, 1:-1]) / (2 * hz)
+    e = eta32.astype(np.float64)
+    vdt2 = (V.astype(np.float64) * dt) ** 2
+    exp = u + vdt2 * (a * gx + b * gy + c * gz) / (1 + e * dt)
+    _, d = _eta_field(nx, ny, nz, w, 1.0)
+    exp[d == 0] = u[d == 0]
+    s = (slice(4, -4),) * 3
+    assert np.abs(exp - u)[s].max() > 1e-2
+    np.testing.assert_allclose(out[s], exp[s], rtol=0, atol=1e-11)
+
+
+def test_stored_eta_zero_equals_profile_eta_zero_bitwise(oracle_lib):
+    s = synth.scenario("RAGGED")
+    sh = (s.nz, s.ny, s.nx)
+    g0 = oracle.make_geom(s.nx, s.ny, s.nz, s.w, s.h, s.dt, 0.0)
+    u0 = synth.random_state(sh, 1)
+    a, ap, _, _ = oracle.propagate(g0, synth.velocity(s), synth.wavelet_for(s, 6), 6, s.source, u0=u0)
+    b, bp, _, _ = oracle.propagate(g0, synth.velocity(s), synth.wavelet_for(s, 6), 6, s.source, u0=u0,
+                                   eta=np.zeros(sh, np.float32))
+    assert np.array_equal(a, b) and np.array_equal(ap, bp)
