@@ -194,6 +194,23 @@ WAVE_API wave_status wave_plan_bind(wave_plan *plan, float *u0, float *u1, float
  * use wave_read / wave_field_ptr. */
 WAVE_API wave_status wave_plan_bind_aux(wave_plan *plan, float *u2, float *u3, void *stream);
 
+/* Stored (user-supplied) PML damping field (the
+ * paper's smem_eta kernels read eta from memory):
+ * bind a caller-owned DEVICE buffer of elems_vdt2 fp32 (vdt2 layout
+ * [nz][ny][pitch_x]); zero-filled.  Single-slab plans only. */
+WAVE_API wave_status wave_plan_bind_eta(wave_plan *plan, float *eta_buf, void *stream);
+
+/* Install eta (dense [nz][ny][nx] fp32 in `where` memory, finite and >= 0;
+ * copied into the bound buffer) instead of the eta_max (d/w)^2 profile; NULL
+ * returns to the profile.  The PML region stays geometric (points with
+ * Chebyshev distance d > 0 to the inner box take the PML update); there eta
+ * is read on the 7-point star from the field (0 outside the domain) and
+ * A = 1 - eta dt, B = 1 + eta dt come from the point's own value, computed in
+ * fp64 and rounded once (R16).  Inner points ignore eta.  The z-PML
+ * caps move from the interior kernel to the wall kernel; two-step blocking is
+ * disabled while a field is installed.  Synchronises `stream`. */
+WAVE_API wave_status wave_set_eta(wave_plan *plan, const float *eta, int32_t where, void *stream);
+
 /* Destroy the plan (caller synchronises its streams first). NULL is a no-op. */
 WAVE_API void wave_plan_destroy(wave_plan *plan);
 

@@ -29,7 +29,7 @@ EXPORTS = [
     "wave_step_finish", "wave_halo_views", "wave_read", "wave_field_ptr", "wave_check_finite",
     "wave_step_index", "wave_get_dt", "wave_launches_per_step", "wave_kernel_points",
     "wave_step_profiled", "wave_set_peers", "wave_step_peer", "wave_push_halo",
-    "wave_plan_bind_aux", "wave_launches", "wave_steps_per_launch",
+    "wave_plan_bind_aux", "wave_launches", "wave_steps_per_launch", "wave_plan_bind_eta", "wave_set_eta",
 ]
 KERNEL_KINDS = ["interior", "xwalls", "ywalls", "source"]
 
@@ -114,6 +114,8 @@ def lib() -> ctypes.CDLL:
                 "wave_plan_bind_aux": ([P, P, P, P], i32),
                 "wave_launches": ([P, i64], i64),
                 "wave_steps_per_launch": ([P], i32),
+                "wave_plan_bind_eta": ([P, P, P], i32),
+                "wave_set_eta": ([P, P, i32, P], i32),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)
@@ -178,6 +180,14 @@ def wave_plan_bind(plan, u0: int, u1: int, vdt2: int, stream: int) -> None:
 
 def wave_plan_bind_aux(plan, u2: int, u3: int, stream: int) -> None:
     check(lib().wave_plan_bind_aux(plan, u2, u3, stream))
+
+
+def wave_plan_bind_eta(plan, eta_buf: int, stream: int) -> None:
+    check(lib().wave_plan_bind_eta(plan, eta_buf, stream))
+
+
+def wave_set_eta(plan, eta_ptr, where: int, stream: int) -> None:
+    check(lib().wave_set_eta(plan, eta_ptr, where, stream))
 
 
 def wave_launches(plan, nsteps: int) -> int:

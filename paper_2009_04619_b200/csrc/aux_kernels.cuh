@@ -14,6 +14,8 @@ struct NaiveParams {
   Coef k;                      // fp32 plans
   CoefT<double> kd;            // fp64 plans
   const void* tab;             // [3][w+2] eta, A, B (T)
+  const float* eta;            // stored (user-supplied) eta [nz][ny][pitch] or null
+  double dt;
 };
 
 template <typename T> __device__ __forceinline__ const CoefT<T>& naive_coef(const NaiveParams& P);
@@ -56,6 +58,18 @@ __global__ void __launch_bounds__(128) k_naive(const T* __restrict__ u, T* __res
   } else {
     const int TN = P.w + 2;
     const T* eta = static_cast<const T*>(P.tab);
+    if (P.eta) {
+      // stored eta: the 7-point star from the field, A/B from the point
+      auto E = [&](int i, int j, int k) -> T {
+        if (i < 0 || i >= P.nx || j < 0 || j >= P.ny || k < 0 || k >= P.nzl) return T(0);
+        return (T)__ldg(P.eta + ((int64_t)k * P.ny + j) * P.pitch + i);
+      };
+      const T g = add_rn(add_rn(gterm(E(x + 1, y, z), E(x - 1, y, z), n.xp[0], n.xm[0], K.i2h[0]),
+                                gterm(E(x, y + 1, z), E(x, y - 1, z), n.yp[0], n.ym[0], K.i2h[1])),
+                         gterm(E(x, y, z + 1), E(x, y, z - 1), n.zp[0], n.zm[0], K.i2h[2]));
+      const double e0 = (double)E(x, y, z);
+      res = upd_pml(L, g, uc, upc, vc, (T)(1.0 - e0 * P.dt), (T)(1.0 + e0 * P.dt));
+    } else {
     const T exp_ = __ldg(eta + max(max(dist1(x + 1, P.nx, P.w), dy), dz));
     const T exm = __ldg(eta + max(max(dist1(x - 1, P.nx, P.w), dy), dz));
     const T eyp = __ldg(eta + max(max(dx, dist1(y + 1, P.ny, P.w)), dz));
@@ -66,6 +80,7 @@ __global__ void __launch_bounds__(128) k_naive(const T* __restrict__ u, T* __res
                               gterm(eyp, eym, n.yp[0], n.ym[0], K.i2h[1])),
                        gterm(ezp, ezm, n.zp[0], n.zm[0], K.i2h[2]));
     res = upd_pml(L, g, uc, upc, vc, __ldg(eta + TN + d), __ldg(eta + 2 * TN + d));
+    }
   }
   up[o] = res;
 }
@@ -184,7 +199,11 @@ __global__ void k_stats(const T* __restrict__ buf, int64_t pitch, int nx, int64_
     const T vt = buf[row * pitch + x];
     if (!isfinite(vt)) { ++bad; continue; }
     const float v = (float)vt;
-    if (!isfinite(v) || (positive_required && !(v > 0.f))) { ++bad; continue; }
+    // positive_required: 1 = must be > 0 (velocity), 2 = must be >= 0 (eta)
+    if (!isfinite(v) || (positive_required == 1 && !(v > 0.f)) || (positive_required == 2 && !(v >= 0.f))) {
+      ++bad;
+      continue;
+    }
     const unsigned int ab = __float_as_uint(fabsf(v));
     mx = max(mx, ab);
     if (v > 0.f) mn = min(mn, __float_as_uint(v));

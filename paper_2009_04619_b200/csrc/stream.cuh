@@ -38,7 +38,8 @@ namespace w25 {
 
 // MODE_FUSED: whole xy plane in one launch, path chosen per warp and plane.
 // MODE_NULL: memory-pattern probe (no stencil; wrong results, diagnostics only).
-enum { MODE_INNER = 0, MODE_WALL = 1, MODE_NULL = 2, MODE_FUSED = 3 };
+// MODE_WALL_ETA: wall kernel reading a stored (user-supplied) eta field.
+enum { MODE_INNER = 0, MODE_WALL = 1, MODE_NULL = 2, MODE_FUSED = 3, MODE_WALL_ETA = 4 };
 
 struct Region {
   int x0, x1, y0, y1, z0, z1;   // point box [x0,x1) x [y0,y1) x [z0,z1) (local z)
@@ -71,6 +72,9 @@ struct StreamParams {
   const CUtensorMap* gu;
   const CUtensorMap* gup;
   const CUtensorMap* gv;
+  // stored (user-supplied) eta: [nz][ny][pitch] fp32 or null
+  const float* eta;
+  double dt;                    // the fp32 dt, widened (A/B = 1 -+ eta dt in fp64)
 };
 
 template <typename T> __device__ __forceinline__ const CoefT<T>& coef_of(const StreamParams& P);
@@ -181,6 +185,43 @@ __device__ __noinline__ typename VecT<T>::V pml_row_call(typename VecT<T>::V L, 
                                 gterm(eyp, eym, vget(yp, c), vget(ym, c), G.i2hy)),
                          gterm(ezp, ezm, vget(zp, c), vget(zm, c), G.i2hz));
       res[c] = upd_pml(Lc, g, uc, upc, vc, stab[G.TN + d], stab[2 * G.TN + d]);
+    }
+  }
+  return vmake<T>(res);
+}
+
+// Stored-eta PML path for one vector row (reading R16): eta on
+// the 7-point star read from the given field (0 outside the domain), A/B =
+// 1 -+ eta dt from the point's own value computed in fp64 and rounded once;
+// points with d = 0 (geometric) take the inner formula.
+template <typename T>
+__device__ __noinline__ typename VecT<T>::V pml_row_eta(typename VecT<T>::V L, typename VecT<T>::V C,
+                                                        typename VecT<T>::V up, typename VecT<T>::V v,
+                                                        typename VecT<T>::V xp, typename VecT<T>::V xm,
+                                                        typename VecT<T>::V yp, typename VecT<T>::V ym,
+                                                        typename VecT<T>::V zp, typename VecT<T>::V zm, int gx,
+                                                        int gy, int z, PmlGeoT<T> G, const float* __restrict__ eta,
+                                                        int64_t pitch, int nzl, double dt) {
+  constexpr int NV = VecT<T>::N;
+  auto E = [&](int x, int y, int zz) -> T {
+    if (x < 0 || x >= G.nx || y < 0 || y >= G.ny || zz < 0 || zz >= nzl) return T(0);
+    return (T)__ldg(eta + ((int64_t)zz * G.ny + y) * pitch + x);
+  };
+  const int dy = dist1(gy, G.ny, G.w), dz = dist1(z, G.nzg, G.w);
+  T res[NV];
+#pragma unroll
+  for (int c = 0; c < NV; ++c) {
+    const int x = gx + c;
+    const int d = max(max(dist1(x, G.nx, G.w), dy), dz);
+    const T uc = vget(C, c), upc = vget(up, c), vc = vget(v, c), Lc = vget(L, c);
+    if (d == 0) {
+      res[c] = upd_inner(Lc, uc, upc, vc);
+    } else {
+      const T g = add_rn(add_rn(gterm(E(x + 1, gy, z), E(x - 1, gy, z), vget(xp, c), vget(xm, c), G.i2hx),
+                                gterm(E(x, gy + 1, z), E(x, gy - 1, z), vget(yp, c), vget(ym, c), G.i2hy)),
+                         gterm(E(x, gy, z + 1), E(x, gy, z - 1), vget(zp, c), vget(zm, c), G.i2hz));
+      const double e0 = (double)E(x, gy, z);
+      res[c] = upd_pml(Lc, g, uc, upc, vc, (T)(1.0 - e0 * dt), (T)(1.0 + e0 * dt));
     }
   }
   return vmake<T>(res);
@@ -358,7 +399,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   T cgr[TYT], Ar[TYT], Br[TYT];              // y-wall: per row
   T cgc[NV], Ac[NV], Bc[NV];                 // x-wall: per column
   // fused mode: warps touching the x/y PML take the same specialised paths
-  const bool wallw = MODE == MODE_WALL || (MODE == MODE_FUSED && warp_xy_pml);
+  const bool wallw = MODE == MODE_WALL || MODE == MODE_WALL_ETA || (MODE == MODE_FUSED && warp_xy_pml);
   if (MODE == MODE_WALL || MODE == MODE_FUSED) {
     bool all_dx0 = true, all_dy0 = true;
 #pragma unroll
@@ -537,6 +578,17 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
                                    Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], cc, K.i2h[0],
                                    K.i2h[1], K.i2h[2]);
           }
+        }
+      } else if (MODE == MODE_WALL_ETA) {
+        // stored (user-supplied) eta: per-point general path, single-slab plans
+#pragma unroll
+        for (int r = 0; r < TYT; ++r) {
+          T xpa[NV], xma[NV];
+#pragma unroll
+          for (int c = 0; c < NV; ++c) { xpa[c] = X[r][XC + c + 1]; xma[c] = X[r][XC + c - 1]; }
+          res[r] = pml_row_eta<T>(vmake<T>(L[r]), Y[R + r], upv[r], vv[r], vmake<T>(xpa), vmake<T>(xma),
+                                  Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], gx, gy + r, z,
+                                  PG, P.eta, P.pitch, P.nzl, P.dt);
         }
       } else if (wallw && wkind != 0 && kg > P.w && kg < P.nzg - P.w - 1) {
         // wall, z-interior plane, pure y-wall rows (g = gy) or pure x-wall

@@ -135,7 +135,9 @@ static KInfo pick(const KInfo* v, int n, const char* env) {
   return v[0];
 }
 
-enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_N = 4 };
+// KI_WALLX_E / KI_WALLY_E: the wall kernels of the stored-eta mode
+enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_WALLX_E = 4, KI_WALLY_E = 5, KI_N = 6 };
+static bool is_wall(int ki) { return ki == KI_WALLX || ki == KI_WALLY || ki == KI_WALLX_E || ki == KI_WALLY_E; }
 
 static KInfo g_k[2][KI_N];   // [precision: 0 fp32, 1 fp64][kernel kind]
 static void init_kernels() {
@@ -156,6 +158,10 @@ static void init_kernels() {
   g_k[1][KI_INNER] = kinfo<124, 124, 8, 1, MODE_INNER, 1, 112, double>("d124x8x1r");
   g_k[1][KI_WALLX] = kinfo<24, 16, 32, 1, MODE_WALL, 1, 0, double>("dx24c16x32x1");
   g_k[1][KI_WALLY] = kinfo<32, 32, 8, 1, MODE_WALL, 3, 0, double>("dy32x8x1m3");
+  g_k[0][KI_WALLX_E] = kinfo<24, 16, 32, 1, MODE_WALL_ETA, 2>("ex24c16x32x1");
+  g_k[0][KI_WALLY_E] = kinfo<64, 64, 8, 1, MODE_WALL_ETA, 3>("ey64x8x1m3");
+  g_k[1][KI_WALLX_E] = kinfo<24, 16, 32, 1, MODE_WALL_ETA, 1, 0, double>("edx24c16x32x1");
+  g_k[1][KI_WALLY_E] = kinfo<32, 32, 8, 1, MODE_WALL_ETA, 3, 0, double>("edy32x8x1m3");
   g_k[1][KI_FUSED] = kinfo<64, 64, 8, 1, MODE_FUSED, 2, 0, double>("dfused64x8x1");
   done = true;
 }
@@ -220,6 +226,8 @@ struct wave_plan {
   float* buf[4] = {nullptr, nullptr, nullptr, nullptr};   // element type by prec (float* = base address)
   float* vdt2 = nullptr;
   bool bound = false, have_vel = false, aux = false;
+  float* eta_buf = nullptr;          // stored eta, caller-owned, vdt2 layout (wave_plan_bind_eta)
+  bool eta_on = false;               // wave_set_eta installed a field
   float dt = 0.f;
   int cur = 0, prv = 1;              // buf[cur] holds u^n, buf[prv] u^{n-1}
   int64_t step = 0;
@@ -234,7 +242,7 @@ struct wave_plan {
   Stats* stats_d = nullptr;
   // launch plans
   Maps maps[KI_N];
-  int occ[KI_N] = {1, 1, 1, 1};
+  int occ[KI_N] = {1, 1, 1, 1, 1, 1};
   bool fused = false;                // WAVE25_FUSED=1: one launch, per-warp paths (measured slower)
   int pf = 1;                        // L2 prefetch distance (WAVE25_PF), measured best
   int prio_lo = 0, prio_hi = 0;      // stream priority range (launch attribute)
@@ -446,14 +454,24 @@ static wave_status build_launches(wave_plan* P) {
       add_regions(P, KI_FUSED, {{0, nx, 0, ny}}, *sets[s], &P->launches[s]);
       continue;
     }
-    // interior kernel: inner xy footprint, all z (z caps plane-uniform)
-    add_regions(P, KI_INNER, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
+    // interior kernel: inner xy footprint, all z (z caps plane-uniform); with a
+    // stored eta the caps are not plane-uniform and go to the wall kernel
+    if (P->eta_on && s == 0 && nz > 2 * w) {
+      add_regions(P, KI_INNER, {{w, nx - w, w, ny - w}}, {{w, nz - w}}, &P->launches[s]);
+      if (w > 0)
+        add_regions(P, KI_WALLY_E, {{w, nx - w, w, ny - w}}, {{0, w}, {nz - w, nz}}, &P->launches[s]);
+    } else if (P->eta_on && s == 0) {
+      add_regions(P, KI_WALLY_E, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
+    } else {
+      add_regions(P, KI_INNER, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
+    }
     // boundary kernels: left/right (x) walls over the full y range (corners
     // included); front/back (y) walls over the inner x range, so that their
     // tiles line up with the interior kernel's wide tiles
     if (w > 0) {
-      add_regions(P, KI_WALLX, {{0, w, 0, ny}, {nx - w, nx, 0, ny}}, *sets[s], &P->launches[s]);
-      add_regions(P, KI_WALLY, {{w, nx - w, 0, w}, {w, nx - w, ny - w, ny}}, *sets[s], &P->launches[s]);
+      const int kx = P->eta_on ? KI_WALLX_E : KI_WALLX, ky = P->eta_on ? KI_WALLY_E : KI_WALLY;
+      add_regions(P, kx, {{0, w, 0, ny}, {nx - w, nx, 0, ny}}, *sets[s], &P->launches[s]);
+      add_regions(P, ky, {{w, nx - w, 0, w}, {w, nx - w, ny - w, ny}}, *sets[s], &P->launches[s]);
     }
   }
   // two-step temporal blocking: interior launch over the (w+4)-shrunk inner xy
@@ -521,6 +539,8 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   p.k = P->coef;
   p.kd = P->coefd;
   p.tab = P->tab_d;
+  p.eta = P->eta_on ? P->eta_buf : nullptr;
+  p.dt = (double)P->dt;
   p.cz = cz;
   p.pf = P->pf;
   p.order = P->order;
@@ -657,6 +677,8 @@ static wave_status launch_naive(wave_plan* P, int cur, int prv, int z0, int z1, 
   np.k = P->coef;
   np.kd = P->coefd;
   np.tab = P->tab_d;
+  np.eta = P->eta_on ? P->eta_buf : nullptr;
+  np.dt = (double)P->dt;
   const dim3 grid((unsigned)((P->d.nx + 31) / 32), (unsigned)((P->d.ny + 3) / 4), (unsigned)(z1 - z0));
   if (P->prec)
     k_naive<double><<<grid, dim3(32, 4), 0, s>>>(reinterpret_cast<const double*>(P->buf[cur]),
@@ -709,20 +731,20 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cu
   // fork BEFORE any launch: the wall kernels (side stream, high priority) and
   // the interior kernel (stream s) run concurrently; join before the source
   bool walls = false;
-  for (const Launch& L : Ls) walls |= (L.ki == KI_WALLX || L.ki == KI_WALLY);
+  for (const Launch& L : Ls) walls |= is_wall(L.ki);
   if (walls && P->serial) {                 // WAVE25_SERIAL=1: everything on `s`, walls first
     for (const Launch& L : Ls)
-      if (L.ki == KI_WALLX || L.ki == KI_WALLY) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+      if (is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
     walls = false;
   }
   if (walls) {
     CK(cudaEventRecord(P->ev_fork, s));
     CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     for (const Launch& L : Ls)
-      if (L.ki == KI_WALLX || L.ki == KI_WALLY) CKST(launch_stream(P, L, cur, prv, P->buf[prv], P->side));
+      if (is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], P->side));
   }
   for (const Launch& L : Ls)
-    if (L.ki != KI_WALLX && L.ki != KI_WALLY) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+    if (!is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
   if (P->serial) return WAVE_OK;
   if (walls) {
     CK(cudaEventRecord(P->ev_join, P->side));
@@ -774,7 +796,7 @@ static wave_status ensure_graph(wave_plan* P, int cur, int prv) {
 // two-step temporal blocking (WAVE_KERNEL_TB2, tb2.cuh)
 // ---------------------------------------------------------------------------
 static bool tb2_active(const wave_plan* P) {
-  return P->d.kernel == WAVE_KERNEL_TB2 && P->aux && P->t2_ok;
+  return P->d.kernel == WAVE_KERNEL_TB2 && P->aux && P->t2_ok && !P->eta_on;
 }
 
 // the two buffers not holding (u^n, u^{n-1}): C gets u^{n+1}, D gets u^{n+2}
@@ -1458,7 +1480,9 @@ float wave_get_dt(const wave_plan* P) { return P ? P->dt : 0.f; }
 
 // measurement kind of a kernel (the fused launch is the interior kind: it is
 // the dominant kernel and covers every point)
-static int kk_of(int ki) { return ki == KI_FUSED ? WAVE_KK_INTERIOR : ki; }
+static int kk_of(int ki) {
+  return ki == KI_FUSED ? WAVE_KK_INTERIOR : ki == KI_WALLX_E ? WAVE_KK_XWALLS : ki == KI_WALLY_E ? WAVE_KK_YWALLS : ki;
+}
 
 static int64_t region_points(const std::vector<Launch>& Ls, int kind) {
   int64_t n = 0;
@@ -1597,6 +1621,40 @@ int64_t wave_launches(const wave_plan* P, int64_t nsteps) {
 int32_t wave_steps_per_launch(const wave_plan* P) {
   if (!P) return -1;
   return tb2_active(P) ? 2 : 1;
+}
+
+wave_status wave_plan_bind_eta(wave_plan* P, float* eta_buf, void* stream) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "bind u0/u1/vdt2 first");
+  if (!eta_buf || reinterpret_cast<uintptr_t>(eta_buf) % 128)
+    return fail(WAVE_ERR_CONFIG, "eta buffer must be a 128-byte aligned device buffer");
+  if (P->d.nz != P->d.nz_global) return fail(WAVE_ERR_CONFIG, "stored eta needs a single-slab plan");
+  CK(cudaMemsetAsync(eta_buf, 0, P->L.elems_vdt2 * sizeof(float), (cudaStream_t)stream));
+  P->eta_buf = eta_buf;
+  P->eta_on = false;
+  return WAVE_OK;
+}
+
+wave_status wave_set_eta(wave_plan* P, const float* eta, int32_t where, void* stream) {
+  if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!eta) {                               // back to the eta_max (d/w)^2 profile
+    P->eta_on = false;
+  } else {
+    if (!P->eta_buf) return fail(WAVE_ERR_STATE, "call wave_plan_bind_eta first");
+    const int64_t rows = P->d.ny * P->d.nz;
+    CK(cudaMemcpy2DAsync(P->eta_buf, P->L.pitch_x * 4, eta, P->d.nx * 4, P->d.nx * 4, rows,
+                         where == WAVE_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+    Stats st;
+    CKST(field_stats(P, P->eta_buf, rows, 2, &st, s));
+    if (st.bad) {
+      P->eta_on = false;
+      return fail(WAVE_ERR_CONFIG, "eta must be finite and >= 0 (%u bad values)", st.bad);
+    }
+    P->eta_on = true;
+  }
+  if (P->dt > 0.f) CKST(build_launches(P));
+  drop_graphs(P);
+  return WAVE_OK;
 }
 
 wave_status wave_plan_bind_aux(wave_plan* P, float* u2, float* u3, void* stream) {

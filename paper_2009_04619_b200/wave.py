@@ -82,6 +82,21 @@ class WavePlan:
             _abi.wave_set_velocity(self._plan, ptr, where, _stream_handle(stream))
         del keep
 
+    def set_eta(self, eta, stream=None) -> None:
+        """Stored (user-supplied) PML damping field eta [nz, ny, nx] (fp32, >= 0)
+        instead of the eta_max (d/w)^2 profile; None returns to the profile.
+        The plan allocates (once) the device buffer the field is copied into."""
+        with torch.cuda.device(self.device):
+            if eta is None:
+                _abi.wave_set_eta(self._plan, None, _abi.WAVE_MEM_HOST, _stream_handle(stream))
+                return
+            if not hasattr(self, "eta_buf"):
+                self.eta_buf = torch.empty(self.layout.elems_vdt2, dtype=torch.float32, device=self.device)
+                _abi.wave_plan_bind_eta(self._plan, self.eta_buf.data_ptr(), _stream_handle(stream))
+            ptr, where, keep = _as_input(eta, self.shape, self.device, torch.float32)
+            _abi.wave_set_eta(self._plan, ptr, where, _stream_handle(stream))
+            del keep
+
     def set_source(self, i, j, k, wavelet, stream=None) -> None:
         wl = np.ascontiguousarray(np.asarray(wavelet, dtype=np.float32).ravel())
         with torch.cuda.device(self.device):
