@@ -11,6 +11,13 @@ steps = int(sys.argv[3]) if len(sys.argv) > 3 else 8
 prec = sys.argv[4] if len(sys.argv) > 4 else "fp32"
 s = synth.scenario(name)
 p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel, precision=prec)
+if os.environ.get("PROF_ETA"):
+    import numpy as np
+    def d1(n):
+        i = np.arange(n)
+        return np.maximum(np.maximum(s.w - i, 0), i - (n - s.w - 1))
+    d = np.maximum(np.maximum(d1(s.nx)[None, None, :], d1(s.ny)[None, :, None]), d1(s.nz)[:, None, None])
+    p.set_eta((s.eta_max * (d / s.w) ** 2).astype(np.float32))
 p.set_velocity(synth.velocity(s))
 p.set_source(*s.source, synth.wavelet_for(s, 4000))
 p.step(4)
