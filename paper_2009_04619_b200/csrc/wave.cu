@@ -99,8 +99,10 @@ static const KInfo* inner_variants(int* n) {
 // x walls: 16 computed columns per tile; 24 + 8 = 32-float (128-B) u boxes
 static const KInfo* wallx_variants(int* n) {
   static const KInfo v[] = {
+      kinfo<24, 16, 128, 1, MODE_WALL, 1, 112>("x24c16x128x1r"),
       kinfo<24, 16, 32, 1, MODE_WALL>("x24c16x32x1"),
       kinfo<28, 16, 32, 1, MODE_WALL>("x28c16x32x1"),
+      kinfo<24, 16, 64, 1, MODE_WALL, 1, 232>("x24c16x64x1r"),
       kinfo<28, 16, 64, 1, MODE_WALL, 1>("x28c16x64x1"),
       kinfo<28, 16, 32, 1, MODE_WALL, 3>("x28c16x32x1m3"),
       kinfo<24, 16, 32, 1, MODE_WALL, 3>("x24c16x32x1m3"),
@@ -116,8 +118,10 @@ static const KInfo* wallx_variants(int* n) {
 
 static const KInfo* wally_variants(int* n) {
   static const KInfo v[] = {
+      kinfo<128, 128, 16, 1, MODE_WALL, 1, 112>("y128x16x1r"),
       kinfo<64, 64, 8, 1, MODE_WALL, 3>("y64x8x1m3"),
       kinfo<248, 248, 8, 1, MODE_WALL, 1, 112>("y248x8x1r"),
+      kinfo<64, 64, 16, 1, MODE_WALL, 2>("y64x16x1m2"),
       kinfo<128, 128, 8, 1, MODE_WALL, 3>("y128x8x1m3"),
       kinfo<128, 128, 8, 1, MODE_WALL, 1>("y128x8x1"),
       kinfo<128, 128, 8, 1, MODE_WALL, 2>("y128x8x1m2"),
@@ -248,6 +252,7 @@ struct wave_plan {
   int prio_lo = 0, prio_hi = 0;      // stream priority range (launch attribute)
   bool wall_prio = true;             // WAVE25_WALL_PRIO=0 disables
   bool serial = false;               // WAVE25_SERIAL=1: walls and interior on one stream (diagnostic)
+  bool xfuse = false;                // WAVE25_XFUSE=1: x walls computed inside the interior tiles
   int order = 0;                     // tile order (WAVE25_ORDER)
   int l2_persist_mb = 0;             // L2 set-aside for u (WAVE25_L2MB), 0 = off
   float l2_hit_ratio = 1.f;          // WAVE25_L2HR
@@ -452,6 +457,13 @@ static wave_status build_launches(wave_plan* P) {
     if (P->fused) {
       // one launch over the whole plane, path per warp
       add_regions(P, KI_FUSED, {{0, nx, 0, ny}}, *sets[s], &P->launches[s]);
+      continue;
+    }
+    if (P->xfuse && !P->eta_on) {
+      // x walls inside the (fused-mode) interior tiles over the full x range;
+      // y walls (corners included) over the full x range
+      add_regions(P, KI_FUSED, {{0, nx, w, ny - w}}, *sets[s], &P->launches[s]);
+      if (w > 0) add_regions(P, KI_WALLY, {{0, nx, 0, w}, {0, nx, ny - w, ny}}, *sets[s], &P->launches[s]);
       continue;
     }
     // interior kernel: inner xy footprint, all z (z caps plane-uniform); with a
@@ -1001,6 +1013,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_PF")) P->pf = atoi(e);
   if (const char* e = getenv("WAVE25_WALL_PRIO")) P->wall_prio = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_SERIAL")) P->serial = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_XFUSE")) P->xfuse = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_GMAPS")) P->gmaps = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
   if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;

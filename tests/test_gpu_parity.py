@@ -378,7 +378,9 @@ for name in ("RAGGED", "C1"):
     {"WAVE25_ABLATION": "st_smem_32x16"}, {"WAVE25_ABLATION": "st_reg_shft_32x16"},
     {"WAVE25_ABLATION": "st_reg_fixed_32x16"}, {"WAVE25_ABLATION": "st_reg_fixed_32x32"},
     {"WAVE25_WALLX_TILE": "x32c16x32x1"}, {"WAVE25_WALLX_TILE": "x24c16x64x1"},
+    {"WAVE25_WALLX_TILE": "x24c16x32x1"}, {"WAVE25_WALLX_TILE": "x24c16x64x1r"},
     {"WAVE25_WALLY_TILE": "y128x8x1"}, {"WAVE25_WALLY_TILE": "y128x16x1"},
+    {"WAVE25_WALLY_TILE": "y64x8x1m3"}, {"WAVE25_XFUSE": "1"},
     {"WAVE25_FUSED": "1"}, {"WAVE25_FORK": "0", "WAVE25_PF": "0"}, {"WAVE25_CZ": "7"},
 ])
 def test_kernel_variants_bitwise(env):
