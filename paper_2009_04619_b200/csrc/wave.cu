@@ -264,6 +264,10 @@ struct wave_plan {
   // streams / graphs
   cudaStream_t side = nullptr, cap = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side2 = nullptr;      // y walls when side2_on (WAVE25_SIDE2)
+  cudaEvent_t ev_join2 = nullptr;
+  bool side2_on = false;
+  int wall_cz = 0;                   // WAVE25_WALL_CZ: wall chunk length (0 = auto)
   cudaGraphExec_t gexec[16] = {};    // 2-step graphs keyed by (cur, prv)
   // two-step temporal blocking (WAVE_KERNEL_TB2)
   T2Info t2{};
@@ -539,6 +543,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   int cz = choose_cz(ncol * (int64_t)zr.size(), nzmax, resident);
   if (ki == KI_INNER)
     if (const char* e = getenv("WAVE25_CZ")) cz = std::max(1, std::min(nzmax, atoi(e)));
+  if (is_wall(ki) && P->wall_cz > 0) cz = std::min(nzmax, P->wall_cz);
 
   Launch Lc;
   Lc.ki = ki;
@@ -752,8 +757,12 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cu
   if (walls) {
     CK(cudaEventRecord(P->ev_fork, s));
     CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
+    if (P->side2_on) CK(cudaStreamWaitEvent(P->side2, P->ev_fork, 0));
     for (const Launch& L : Ls)
-      if (is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], P->side));
+      if (is_wall(L.ki)) {
+        const bool y = L.ki == KI_WALLY || L.ki == KI_WALLY_E;
+        CKST(launch_stream(P, L, cur, prv, P->buf[prv], (y && P->side2_on) ? P->side2 : P->side));
+      }
   }
   for (const Launch& L : Ls)
     if (!is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
@@ -761,6 +770,10 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cu
   if (walls) {
     CK(cudaEventRecord(P->ev_join, P->side));
     CK(cudaStreamWaitEvent(s, P->ev_join, 0));
+    if (P->side2_on) {
+      CK(cudaEventRecord(P->ev_join2, P->side2));
+      CK(cudaStreamWaitEvent(s, P->ev_join2, 0));
+    }
   }
   return WAVE_OK;
 }
@@ -1014,6 +1027,8 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_WALL_PRIO")) P->wall_prio = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_SERIAL")) P->serial = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_XFUSE")) P->xfuse = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_SIDE2")) P->side2_on = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
   if (const char* e = getenv("WAVE25_GMAPS")) P->gmaps = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
   if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;
@@ -1039,7 +1054,9 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if ((e = cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&P->cap, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
-      (e = cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+      (e = cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaStreamCreateWithFlags(&P->side2, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&P->ev_join2, cudaEventDisableTiming)) != cudaSuccess)
     return bail(fail(WAVE_ERR_CUDA, "stream/event: %s", cudaGetErrorString(e)));
   for (int ki = 0; ki < KI_N; ++ki) {
     const size_t sm = kernel_smem(P, ki);
@@ -1080,6 +1097,8 @@ void wave_plan_destroy(wave_plan* P) {
   if (P->cap) cudaStreamDestroy(P->cap);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join) cudaEventDestroy(P->ev_join);
+  if (P->side2) cudaStreamDestroy(P->side2);
+  if (P->ev_join2) cudaEventDestroy(P->ev_join2);
   delete P;
 }
 
