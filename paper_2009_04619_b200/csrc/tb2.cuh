@@ -193,7 +193,9 @@ k_tb2(const __grid_constant__ CUtensorMap tm_u,    // A = u^n, box (W0, H0, 1)
       mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], C::NW2);
     }
 #pragma unroll
-    for (int s = 0; s < C::NU1; ++s) { mbar_init(&full_1[s], C::NWC); mbar_init(&empty_1[s], C::NW2); }
+    // U1 (thread-written, read by other warps): every writer thread arrives
+    // (release of its own store), so the reader's acquire covers each store
+    for (int s = 0; s < C::NU1; ++s) { mbar_init(&full_1[s], C::NWC * 32); mbar_init(&empty_1[s], C::NW2 * 32); }
     fence_mbar_init();
   }
   const int TABN = P.w + 2;
@@ -346,8 +348,7 @@ k_tb2(const __grid_constant__ CUtensorMap tm_u,    // A = u^n, box (W0, H0, 1)
           const int slot = u1w % C::NU1, use = u1w / C::NU1;
           if (use > 0) mbar_wait(&empty_1[slot], (use - 1) & 1);
           *reinterpret_cast<float4*>(su1 + slot * C::S1S + po) = u1;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full_1[slot]);
+          mbar_arrive(&full_1[slot]);
           ++u1w;
         }
         q2[s] = u1;                               // slot i % 9 = s
@@ -374,8 +375,9 @@ k_tb2(const __grid_constant__ CUtensorMap tm_u,    // A = u^n, box (W0, H0, 1)
         const int sv = iv % SP;
         mbar_wait(&full_v[sv], (iv / SP) & 1);
         const float4 vv = lds4(sv2 + sv * C::S2S + vo);
+        mbar_arrive(&empty_1[slot]);
         __syncwarp();
-        if (lane == 0) { mbar_arrive(&empty_1[slot]); mbar_arrive(&empty_v[sv]); }
+        if (lane == 0) mbar_arrive(&empty_v[sv]);
         ++u1r;
         const float4 upv = q1[s % 9];             // u^n(z2): the oldest q1 slot
         const int kg = z2 + P.zoff;

@@ -1,22 +1,38 @@
-"""Small end-to-end runs for compute-sanitizer (development aid): C1 and RAGGED
-geometries, stream + naive kernels, graph replay, slab split path."""
+"""Small end-to-end runs for compute-sanitizer (development aid): every kernel
+family (stream / naive / tb2), fp32 and fp64, stored eta, the paper-shape
+ablation kernels, graph replay and the slab split path, on C1 / RAGGED-size
+grids."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth
 from paper_2009_04619_b200.wave import WavePlan
 
-for name, kw in [("C1", {}), ("RAGGED", {}), ("RAGGED", dict(nx=9, ny=11, nz=10, w=2, src=(4, 5, 5)))]:
+
+def run(s, kernel="stream", precision="fp32", eta=False, steps=5):
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel, precision=precision)
+    if eta:
+        p.set_eta(np.full((s.nz, s.ny, s.nx), 2.0, np.float32))
+    p.set_velocity(synth.velocity(s))
+    p.set_source(*s.source, synth.wavelet_for(s, 8))
+    u0 = synth.random_state((s.nz, s.ny, s.nx), 1)
+    p.set_state(None, u0 if precision == "fp32" else u0.astype(np.float64))
+    p.step(steps)
+    p.check_finite()
+    _ = p.read(0).cpu()
+    p.close()
+
+
+cases = [("C1", {}), ("RAGGED", {}), ("RAGGED", dict(nx=9, ny=11, nz=10, w=2, src=(4, 5, 5)))]
+for name, kw in cases:
     s = synth.scenario(name, **kw)
-    for kernel in ("stream", "naive"):
-        p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel)
-        p.set_velocity(synth.velocity(s))
-        p.set_source(*s.source, synth.wavelet_for(s, 8))
-        p.set_state(None, synth.random_state((s.nz, s.ny, s.nx), 1))
-        p.step(5)
-        p.check_finite()
-        _ = p.read(0).cpu()
-        p.close()
+    for kernel in ("stream", "naive", "tb2"):
+        run(s, kernel)
+    run(s, "stream", "fp64")
+    run(s, "naive", "fp64")
+    run(s, "stream", eta=True)
+if os.environ.get("WAVE25_ABLATION"):
+    run(synth.scenario("RAGGED"), "stream")
 # slab split path
 s = synth.scenario("RAGGED")
 p = WavePlan(s.nx, s.ny, 30, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=0)
