@@ -304,6 +304,20 @@ static wave_status get_encoder() {
   return WAVE_OK;
 }
 
+// L2 sector promotion of TMA loads (WAVE25_L2PROMO = 0 none, 1 64B, 2 128B, 3 256B)
+static CUtensorMapL2promotion l2_promotion() {
+  static int v = [] {
+    const char* e = getenv("WAVE25_L2PROMO");
+    return e ? atoi(e) : 2;
+  }();
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 3: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  }
+}
+
 static wave_status encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                             uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t b0, uint32_t b1,
                             bool f64 = false) {
@@ -313,8 +327,8 @@ static wave_status encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = g_encode(m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
                         dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(WAVE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return WAVE_OK;
 }
