@@ -127,3 +127,28 @@ def test_no_cpu_fallback_when_library_missing(tmp_path, monkeypatch):
     monkeypatch.setattr(_abi, "_lib", None)
     with pytest.raises(ImportError):
         _abi.lib()
+
+
+def test_layout_fp64_element_size():
+    d32 = _abi.make_desc(70, 45, 53, 5, 7.5, 6e-4)
+    d64 = _abi.make_desc(70, 45, 53, 5, 7.5, 6e-4, precision=_abi.WAVE_PREC_FP64)
+    l32, l64 = _abi.wave_layout(d32), _abi.wave_layout(d64)
+    assert l32.elem_bytes == 4 and l64.elem_bytes == 8
+    # same element counts: the layout is in elements of the plan's precision
+    assert (l32.pitch_x, l32.elems_u, l32.elems_vdt2) == (l64.pitch_x, l64.elems_u, l64.elems_vdt2)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(precision=2), "precision"),
+    (dict(precision=_abi.WAVE_PREC_FP64, kernel=_abi.WAVE_KERNEL_TB2), "TB2"),
+])
+def test_precision_validation(kw, msg):
+    d = _abi.make_desc(70, 45, 53, 5, 7.5, 6e-4, **kw)
+    with pytest.raises(_abi.WaveError) as ei:
+        _abi.wave_layout(d)
+    assert ei.value.status == _abi.WAVE_ERR_CONFIG and msg in ei.value.message
+
+
+def test_host_only_calls_accept_tb2_fp32():
+    d = _abi.make_desc(70, 45, 53, 5, 7.5, 6e-4, kernel=_abi.WAVE_KERNEL_TB2)
+    assert _abi.wave_layout(d).elems_u == 61 * 45 * 72
