@@ -13,6 +13,8 @@
 //   st_reg_shft     2.5-D streaming, xy plane in shared memory, z window in 9
 //                   registers shifted every plane (L666-717)
 //   st_reg_fixed    same with fixed registers and the loop unrolled 9x (L735-775)
+//   semi            streaming with the semi-stencil along z (L580-617); not
+//                   bitwise (different summation order), within the 1e-5 gate
 #pragma once
 #include "stream.cuh"
 
@@ -221,6 +223,68 @@ __global__ void __launch_bounds__(DX * DY) k_st(const AblParams P) {
           __syncthreads();
         }
       }
+    }
+  }
+}
+
+// ---- semi: 2.5-D streaming with the semi-stencil along z (PAPER.md L580-617,
+// after de la Cruz et al.).  Every plane value, as soon as it is loaded,
+// scatters its z contributions c_zm u(q) into the partial sums of the 2R points
+// q-R..q-1 and q+1..q+R it belongs to; the x/y part of point q is added when
+// plane q is in shared memory; point q-R is complete.  One load per plane, a
+// 2R+1-slot ring of partial sums instead of values.  The summation order
+// differs from Eq. 3's (forward/backward halves), so this shape is compared
+// with the oracle within the 1e-5 gate, not bitwise.
+template <int DX, int DY, bool CHK>
+__global__ void __launch_bounds__(DX * DY) k_semi(const AblParams P) {
+  constexpr int W = DX + 2 * R, NS = 2 * R + 1;
+  __shared__ float B[W * (DY + 2 * R)];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int xb = P.x0 + blockIdx.x * DX, yb = P.y0 + blockIdx.y * DY;
+  const int x = xb + tx, y = yb + ty;
+  const bool act = x < P.x1 && y < P.y1;
+  const int o = (ty + R) * W + tx + R;
+  float A[NS];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) A[i] = 0.f;
+  // slot of plane p: (p - (z0 - R)) % NS; iteration q runs from z0-R to z1+R-1
+#pragma unroll 1
+  for (int q0 = P.z0 - R; q0 < P.z1 + R; q0 += NS) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const int q = q0 + s;
+      if (q >= P.z1 + R) break;
+      const float val = abl_u<CHK>(P, x, y, q);
+      const bool inq = q >= P.z0 && q < P.z1;          // block-uniform
+      if (inq) {
+        st_load_plane<DX, DY, CHK>(P, B, xb, yb, q, tx, ty, true, val);
+        __syncthreads();
+        float xy = __fmul_rn(P.k.c0, val);
+#pragma unroll
+        for (int m = 1; m <= R; ++m) xy = __fmaf_rn(P.k.cx[m - 1], __fadd_rn(B[o + m], B[o - m]), xy);
+#pragma unroll
+        for (int m = 1; m <= R; ++m) xy = __fmaf_rn(P.k.cy[m - 1], __fadd_rn(B[o + m * W], B[o - m * W]), xy);
+        A[s] = __fadd_rn(A[s], xy);
+        __syncthreads();
+      }
+      // scatter u(q) into the partial sums of q-m (forward half) and q+m (backward half)
+#pragma unroll
+      for (int m = 1; m <= R; ++m) {
+        A[(s - m + NS) % NS] = __fmaf_rn(P.k.cz[m - 1], val, A[(s - m + NS) % NS]);
+        A[(s + m) % NS] = __fmaf_rn(P.k.cz[m - 1], val, A[(s + m) % NS]);
+      }
+      // point p = q - R is complete
+      const int p = q - R;
+      const int sp = (s - R + NS) % NS;
+      if (act && p >= P.z0 && p < P.z1) {
+        Nbr n;
+        const float c = abl_u<CHK>(P, x, y, p);
+        n.xp[0] = abl_u<CHK>(P, x + 1, y, p); n.xm[0] = abl_u<CHK>(P, x - 1, y, p);
+        n.yp[0] = abl_u<CHK>(P, x, y + 1, p); n.ym[0] = abl_u<CHK>(P, x, y - 1, p);
+        n.zp[0] = abl_u<CHK>(P, x, y, p + 1); n.zm[0] = abl_u<CHK>(P, x, y, p - 1);
+        abl_store(P, x, y, p, A[sp], c, n);
+      }
+      A[sp] = 0.f;                                      // slot reused by plane q + R + 1
     }
   }
 }

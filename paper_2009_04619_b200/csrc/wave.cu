@@ -621,6 +621,7 @@ static bool launch_shape(const char* sh, const AblParams& a, int ex, int ey, int
   else if (!strcmp(sh, "st_reg_shft_32x16")) k_st<ST_SHFT, 32, 16, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 16)), dim3(32, 16), 0, s>>>(a);
   else if (!strcmp(sh, "st_reg_fixed_32x16")) k_st<ST_FIXED, 32, 16, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 16)), dim3(32, 16), 0, s>>>(a);
   else if (!strcmp(sh, "st_reg_fixed_32x32")) k_st<ST_FIXED, 32, 32, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 32)), dim3(32, 32), 0, s>>>(a);
+  else if (!strcmp(sh, "semi_32x16")) k_semi<32, 16, CHK><<<dim3(cdiv(ex, 32), cdiv(ey, 16)), dim3(32, 16), 0, s>>>(a);
   else return false;
   return true;
 }

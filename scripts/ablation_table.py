@@ -1,7 +1,7 @@
 """Summarise the code-shape ablation ncu CSVs (scripts/ablation_ncu.sh) into a table."""
 import csv, sys
 order = ["default", "gmem_32x4x1", "gmem_8x8x8", "smem_u", "st_smem_32x16", "st_reg_shft_32x16",
-         "st_reg_fixed_32x16", "st_reg_fixed_32x32"]
+         "st_reg_fixed_32x16", "st_reg_fixed_32x32", "semi_32x16"]
 pts = 1007681536
 d0 = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out"
 print(f"{'shape':22s} {'ms(ncu)':>8s} {'DRAM B/pt':>9s} {'inst/pt':>8s} {'regs':>5s} {'warps%':>7s} {'issue%':>7s} {'smem wf/pt':>10s} {'L2hit%':>7s}")
