@@ -83,6 +83,7 @@ static const KInfo* inner_variants(int* n) {
       kinfo<128, 128, 8, 1, MODE_FUSED>("fused128x8x1"),
       kinfo<128, 128, 16, 1, MODE_NULL, 1>("null128x16x1"),
       kinfo<248, 248, 8, 1, MODE_INNER, 1>("248x8x1"),
+      kinfo<240, 240, 8, 1, MODE_INNER, 1, 112>("240x8x1r"),
       kinfo<256, 256, 8, 1, MODE_INNER, 1, 112>("256x8x1r"),
       kinfo<248, 248, 8, 2, MODE_INNER, 1>("248x8x2"),
       kinfo<248, 248, 4, 1, MODE_INNER, 1>("248x4x1"),
@@ -103,6 +104,7 @@ static const KInfo* wallx_variants(int* n) {
       kinfo<24, 16, 32, 1, MODE_WALL>("x24c16x32x1"),
       kinfo<28, 16, 32, 1, MODE_WALL>("x28c16x32x1"),
       kinfo<24, 16, 64, 1, MODE_WALL, 1, 232>("x24c16x64x1r"),
+      kinfo<40, 32, 64, 1, MODE_WALL, 1, 112>("x40c32x64x1r"),
       kinfo<28, 16, 64, 1, MODE_WALL, 1>("x28c16x64x1"),
       kinfo<28, 16, 32, 1, MODE_WALL, 3>("x28c16x32x1m3"),
       kinfo<24, 16, 32, 1, MODE_WALL, 3>("x24c16x32x1m3"),
@@ -268,6 +270,7 @@ struct wave_plan {
   cudaEvent_t ev_join2 = nullptr;
   bool side2_on = false;
   int wall_cz = 0;                   // WAVE25_WALL_CZ: wall chunk length (0 = auto)
+  int xwall_extra = 0;               // WAVE25_XWALL_EXTRA: inner columns computed by the x-wall kernel
   cudaGraphExec_t gexec[16] = {};    // 2-step graphs keyed by (cur, prv)
   // two-step temporal blocking (WAVE_KERNEL_TB2)
   T2Info t2{};
@@ -493,15 +496,17 @@ static wave_status build_launches(wave_plan* P) {
     } else if (P->eta_on && s == 0) {
       add_regions(P, KI_WALLY_E, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
     } else {
-      add_regions(P, KI_INNER, {{w, nx - w, w, ny - w}}, *sets[s], &P->launches[s]);
+      const int xw = w > 0 ? w + P->xwall_extra : 0;
+      add_regions(P, KI_INNER, {{xw, nx - xw, w, ny - w}}, *sets[s], &P->launches[s]);
     }
     // boundary kernels: left/right (x) walls over the full y range (corners
     // included); front/back (y) walls over the inner x range, so that their
     // tiles line up with the interior kernel's wide tiles
     if (w > 0) {
       const int kx = P->eta_on ? KI_WALLX_E : KI_WALLX, ky = P->eta_on ? KI_WALLY_E : KI_WALLY;
-      add_regions(P, kx, {{0, w, 0, ny}, {nx - w, nx, 0, ny}}, *sets[s], &P->launches[s]);
-      add_regions(P, ky, {{w, nx - w, 0, w}, {w, nx - w, ny - w, ny}}, *sets[s], &P->launches[s]);
+      const int xw = w + P->xwall_extra;          // x-wall width (>= w: extra inner columns)
+      add_regions(P, kx, {{0, xw, 0, ny}, {nx - xw, nx, 0, ny}}, *sets[s], &P->launches[s]);
+      add_regions(P, ky, {{xw, nx - xw, 0, w}, {xw, nx - xw, ny - w, ny}}, *sets[s], &P->launches[s]);
     }
   }
   // two-step temporal blocking: interior launch over the (w+4)-shrunk inner xy
@@ -1044,6 +1049,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_XFUSE")) P->xfuse = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_SIDE2")) P->side2_on = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
+  if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
   if (const char* e = getenv("WAVE25_GMAPS")) P->gmaps = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
   if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;
