@@ -271,6 +271,7 @@ struct wave_plan {
   bool side2_on = false;
   int wall_cz = 0;                   // WAVE25_WALL_CZ: wall chunk length (0 = auto)
   int xwall_extra = 0;               // WAVE25_XWALL_EXTRA: inner columns computed by the x-wall kernel
+  bool walls_last = false;           // WAVE25_WALLS_LAST: enqueue the wall kernels after the interior
   cudaGraphExec_t gexec[16] = {};    // 2-step graphs keyed by (cur, prv)
   // two-step temporal blocking (WAVE_KERNEL_TB2)
   T2Info t2{};
@@ -774,18 +775,23 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cu
       if (is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
     walls = false;
   }
-  if (walls) {
-    CK(cudaEventRecord(P->ev_fork, s));
-    CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
-    if (P->side2_on) CK(cudaStreamWaitEvent(P->side2, P->ev_fork, 0));
+  auto launch_walls = [&]() -> wave_status {
     for (const Launch& L : Ls)
       if (is_wall(L.ki)) {
         const bool y = L.ki == KI_WALLY || L.ki == KI_WALLY_E;
         CKST(launch_stream(P, L, cur, prv, P->buf[prv], (y && P->side2_on) ? P->side2 : P->side));
       }
+    return WAVE_OK;
+  };
+  if (walls) {
+    CK(cudaEventRecord(P->ev_fork, s));
+    CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
+    if (P->side2_on) CK(cudaStreamWaitEvent(P->side2, P->ev_fork, 0));
+    if (!P->walls_last) CKST(launch_walls());
   }
   for (const Launch& L : Ls)
     if (!is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+  if (walls && P->walls_last) CKST(launch_walls());
   if (P->serial) return WAVE_OK;
   if (walls) {
     CK(cudaEventRecord(P->ev_join, P->side));
@@ -1050,6 +1056,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_SIDE2")) P->side2_on = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
+  if (const char* e = getenv("WAVE25_WALLS_LAST")) P->walls_last = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_GMAPS")) P->gmaps = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
   if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;
