@@ -34,10 +34,10 @@ def rel_linf(got, ref):
     return float(np.abs(got.astype(np.float64) - ref).max()) / (m if m > 0 else 1.0)
 
 
-def run_gpu(s, steps, u0=None, um1=None, kernel="stream", V=None, wl=None):
+def run_gpu(s, steps, u0=None, um1=None, kernel="stream", V=None, wl=None, precision="fp32"):
     V = synth.velocity(s) if V is None else V
     wl = synth.wavelet_for(s, max(steps, 1)) if wl is None else wl
-    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel)
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel, precision=precision)
     p.set_velocity(V)
     p.set_source(*s.source, wl)
     if u0 is not None or um1 is not None:
@@ -163,19 +163,22 @@ def test_graph_replay_matches_stepwise():
     assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("nslab", [2, 3])
-def test_slabs_on_one_gpu_bitwise(nslab):
+@pytest.mark.parametrize("nslab,precision", [(2, "fp32"), (3, "fp32"), (2, "fp64")])
+def test_slabs_on_one_gpu_bitwise(nslab, precision):
     # z-slab plans + edges/interior split + device-to-device halo exchange == single plan
     from paper_2009_04619_b200.dist import slab_bounds
     s = synth.scenario("RAGGED")
     sh = (s.nz, s.ny, s.nx)
     u0, um1 = synth.random_state(sh, 7), synth.random_state(sh, 8)
+    if precision == "fp64":
+        u0, um1 = u0.astype(np.float64), um1.astype(np.float64)
     V = synth.velocity(s)
     wl = synth.wavelet_for(s, 25)
     plans = []
     for r in range(nslab):
         off, nzl = slab_bounds(s.nz, r, nslab)
-        p = WavePlan(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
+        p = WavePlan(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off,
+                     precision=precision)
         p.set_velocity(V[off:off + nzl])
         p.set_source(*s.source, wl)
         p.set_state(um1[off:off + nzl], u0[off:off + nzl])
@@ -184,7 +187,8 @@ def test_slabs_on_one_gpu_bitwise(nslab):
     for r, (p, off, nzl) in enumerate(plans):
         cur = p.field(0)
         full = torch.from_numpy(u0).cuda()
-        buf = [b for b in p.bufs if b.data_ptr() <= cur.data_ptr() < b.data_ptr() + 4 * b.numel()][0]
+        buf = [b for b in p.bufs
+               if b.data_ptr() <= cur.data_ptr() < b.data_ptr() + b.element_size() * b.numel()][0]
         plane = s.ny * p.layout.pitch_x
         v = buf.view(-1, s.ny, p.layout.pitch_x)
         if r > 0:
@@ -204,7 +208,7 @@ def test_slabs_on_one_gpu_bitwise(nslab):
             p.step_interior()
             p.step_finish()
     got = np.concatenate([p.read(0).cpu().numpy() for p, _, _ in plans], axis=0)
-    ref, _ = run_gpu(s, 25, u0, um1, wl=wl)
+    ref, _ = run_gpu(s, 25, u0, um1, wl=wl, precision=precision)
     for p, _, _ in plans:
         p.close()
     assert np.array_equal(got, ref)
