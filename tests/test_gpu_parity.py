@@ -246,7 +246,7 @@ def test_auto_dt_matches_oracle_rule():
     p.close()
 
 
-def _full_size_slab_check(sname, steps, zt_list, seed=0):
+def _full_size_slab_check(sname, steps, zt_list, seed=0, kernel="stream"):
     """Full-size GPU run; oracle recomputes sampled z-slabs.  The oracle slab
     is the target planes plus 4*steps planes of margin on each side, whose
     ghost planes hold the initial state: after `steps` steps the target planes
@@ -257,11 +257,12 @@ def _full_size_slab_check(sname, steps, zt_list, seed=0):
     um1 = synth.random_state(sh, seed + 1)
     V = synth.velocity(s)
     wl = synth.wavelet_for(s, steps)
-    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel)
     p.set_velocity(V)
     p.set_source(*s.source, wl)
     p.set_state(um1, u0)
     p.step(steps)
+    assert kernel != "tb2" or p.steps_per_launch == 2
     gpu = p.field(0)
     R = 4
     M = R * steps
@@ -288,15 +289,15 @@ def _full_size_slab_check(sname, steps, zt_list, seed=0):
     return worst
 
 
-@pytest.mark.parametrize("sname", ["C2", "C3"])
-def test_full_size_sampled_slabs(sname):
+@pytest.mark.parametrize("sname,kernel", [("C2", "stream"), ("C3", "stream"), ("C2", "tb2"), ("C3", "tb2")])
+def test_full_size_sampled_slabs(sname, kernel):
     # BASELINE.json configs[1] / configs[2] at full size, the bench's launch
     # configuration (stream kernels, CUDA graphs); sampled z ranges cover the
     # top cap, the middle (source plane) and the bottom cap.
     s = synth.scenario(sname)
     n = s.nz
     zt = [(0, 6), (n // 2 - 3, n // 2 + 3), (n - 6, n)]
-    err = _full_size_slab_check(sname, 5, zt)
+    err = _full_size_slab_check(sname, 6 if kernel == "tb2" else 5, zt, kernel=kernel)
     assert err <= TOL, err
 
 
