@@ -1225,7 +1225,8 @@ static wave_status field_stats(wave_plan* P, const float* base, int64_t rows, in
   Stats init{0u, 0x7f7fffffu, 0u, 0u};
   CK(cudaMemcpyAsync(P->stats_d, &init, sizeof init, cudaMemcpyHostToDevice, s));
   const int64_t n = rows * P->d.nx;
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 4 * 148 * 8));
+  (void)n;
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(rows, 148 * 16));
   if (f64)
     k_stats<double><<<blocks, 256, 0, s>>>(reinterpret_cast<const double*>(base), P->L.pitch_x, (int)P->d.nx, rows,
                                            positive, P->stats_d);
@@ -1265,10 +1266,12 @@ wave_status wave_set_velocity(wave_plan* P, const float* vel, int32_t where, voi
   if (cn > 1.0) return fail(WAVE_ERR_CONFIG, "dt = %g violates the Courant limit (ratio %.4f > 1)", dt, cn);
   P->dt = dt;
   if (P->prec)
-    k_vdt2<double><<<4 * 148, 256, 0, s>>>(reinterpret_cast<double*>(P->vdt2), vbuf, P->L.pitch_x, (int)P->d.nx, rows,
+    k_vdt2<double><<<(unsigned)std::min<int64_t>(rows, 148 * 16), 256, 0, s>>>(reinterpret_cast<double*>(P->vdt2), vbuf,
+                                                                             P->L.pitch_x, (int)P->d.nx, rows,
                                            (double)dt);
   else
-    k_vdt2<float><<<4 * 148, 256, 0, s>>>(P->vdt2, vbuf, P->L.pitch_x, (int)P->d.nx, rows, (double)dt);
+    k_vdt2<float><<<(unsigned)std::min<int64_t>(rows, 148 * 16), 256, 0, s>>>(P->vdt2, vbuf, P->L.pitch_x,
+                                                                            (int)P->d.nx, rows, (double)dt);
   CK(cudaGetLastError());
   CKST(refresh_tables(P, s));
   P->have_vel = true;
