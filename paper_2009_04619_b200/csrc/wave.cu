@@ -162,8 +162,14 @@ static void init_kernels() {
   // fp64: 16-B lanes hold 2 doubles; 124 = 992 / 8 columns,
   // u box 132 doubles; same ring / warpgroup structure as the fp32 kernels
   g_k[1][KI_INNER] = kinfo<124, 124, 8, 1, MODE_INNER, 1, 112, double>("d124x8x1r");
-  g_k[1][KI_WALLX] = kinfo<24, 16, 32, 1, MODE_WALL, 1, 0, double>("dx24c16x32x1");
-  g_k[1][KI_WALLY] = kinfo<32, 32, 8, 1, MODE_WALL, 3, 0, double>("dy32x8x1m3");
+  {
+    static const KInfo dx[] = {kinfo<24, 16, 64, 1, MODE_WALL, 1, 112, double>("dx24c16x64x1r"),
+                               kinfo<24, 16, 32, 1, MODE_WALL, 1, 0, double>("dx24c16x32x1")};
+    static const KInfo dy[] = {kinfo<64, 64, 16, 1, MODE_WALL, 1, 112, double>("dy64x16x1r"),
+                               kinfo<32, 32, 8, 1, MODE_WALL, 3, 0, double>("dy32x8x1m3")};
+    g_k[1][KI_WALLX] = pick(dx, 2, "WAVE25_DWALLX_TILE");
+    g_k[1][KI_WALLY] = pick(dy, 2, "WAVE25_DWALLY_TILE");
+  }
   g_k[0][KI_WALLX_E] = kinfo<24, 16, 32, 1, MODE_WALL_ETA, 2>("ex24c16x32x1");
   g_k[0][KI_WALLY_E] = kinfo<64, 64, 8, 1, MODE_WALL_ETA, 3>("ey64x8x1m3");
   g_k[1][KI_WALLX_E] = kinfo<24, 16, 32, 1, MODE_WALL_ETA, 1, 0, double>("edx24c16x32x1");
