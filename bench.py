@@ -352,7 +352,8 @@ def run_ours(args, rank, world, local):
         step_ms_prof = sum(kms.values()) / max(args.steps, 1)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": ncu_traffic("interior") if (args.precision == "fp32" and args.kernel == "stream") else None,
-                "kernel": ("k_tb2 interior (two-step temporal blocking)" if plan.steps_per_launch == 2
+                "kernel": ("k_tb2 interior (two-step temporal blocking)" if args.kernel == "tb2"
+                           else "k_stream PAIR interior (two steps through L2)" if args.kernel == "pair"
                            else "k_stream interior (TMA z-streaming, 25-pt)"),
                 "points_per_launch": kpts["interior"], "bytes_per_point": bpl,
                 "ms_per_launch": t_launch, "peak_source": peak_src,
@@ -436,7 +437,7 @@ def main():
     ap.add_argument("--no-probe", action="store_true")
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--repeats", type=int, default=5, help="timed runs (the first is `value`)")
-    ap.add_argument("--kernel", choices=["stream", "tb2"], default="stream",
+    ap.add_argument("--kernel", choices=["stream", "tb2", "pair"], default="stream",
                     help="1 GPU: stream (default) or tb2 two-step temporal blocking")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

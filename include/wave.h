@@ -74,7 +74,13 @@ typedef enum { WAVE_MEM_HOST = 0, WAVE_MEM_DEVICE = 1 } wave_mem;
  * it needs two extra wavefield buffers (wave_plan_bind_aux) and a single-slab
  * plan, and falls back to STREAM single steps otherwise (odd step counts end
  * with one STREAM step).  All three compute bitwise-identical values. */
-typedef enum { WAVE_KERNEL_STREAM = 0, WAVE_KERNEL_NAIVE = 1, WAVE_KERNEL_TB2 = 2 } wave_kernel;
+typedef enum { WAVE_KERNEL_STREAM = 0, WAVE_KERNEL_NAIVE = 1, WAVE_KERNEL_TB2 = 2, WAVE_KERNEL_PAIR = 3 } wave_kernel;
+/* WAVE_KERNEL_PAIR: two steps per interior launch with no
+ * redundant work: step-1 blocks publish per-plane progress, step-2 blocks of
+ * the same launch wait for their own and neighbouring tiles and read u^{n+1}
+ * back through L2; walls run as single steps before and after.  In place
+ * (two buffers), single-slab plans, falls back to STREAM with a stored eta.
+ * Bitwise equal to STREAM. */
 
 /* Arithmetic / storage precision of a plan.  FP32 (default): every constant
  * computed in fp64 and rounded once to fp32 (R8), fp32 storage and

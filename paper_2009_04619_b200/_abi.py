@@ -18,7 +18,7 @@ WAVE_OK, WAVE_ERR_CONFIG, WAVE_ERR_UNSTABLE, WAVE_ERR_VERIFY, WAVE_ERR_CUDA, WAV
 STATUS_NAMES = {0: "WAVE_OK", 1: "WAVE_ERR_CONFIG", 2: "WAVE_ERR_UNSTABLE", 3: "WAVE_ERR_VERIFY",
                 4: "WAVE_ERR_CUDA", 5: "WAVE_ERR_ALLOC", 6: "WAVE_ERR_STATE"}
 WAVE_MEM_HOST, WAVE_MEM_DEVICE = 0, 1
-WAVE_KERNEL_STREAM, WAVE_KERNEL_NAIVE, WAVE_KERNEL_TB2 = 0, 1, 2
+WAVE_KERNEL_STREAM, WAVE_KERNEL_NAIVE, WAVE_KERNEL_TB2, WAVE_KERNEL_PAIR = 0, 1, 2, 3
 WAVE_PREC_FP32, WAVE_PREC_FP64 = 0, 1
 REGION_NAMES = ["inner", "top", "bottom", "front", "back", "left", "right"]
 

@@ -103,10 +103,11 @@ __global__ void k_source(T* __restrict__ buf, int64_t off, const T* __restrict__
 
 // Source into a value computed by a wall kernel of a two-step pair:
 // buf[off] += inc[n + delta], n = the device step counter (not advanced).
-__global__ void k_source_at(float* __restrict__ buf, int64_t off, const float* __restrict__ inc, int64_t ninc,
+template <typename T>
+__global__ void k_source_at(T* __restrict__ buf, int64_t off, const T* __restrict__ inc, int64_t ninc,
                             const unsigned long long* __restrict__ dstep, int delta) {
   const unsigned long long n = *dstep + (unsigned long long)delta;
-  if (n < (unsigned long long)ninc) buf[off] = __fadd_rn(buf[off], inc[n]);
+  if (n < (unsigned long long)ninc) buf[off] = add_rn(buf[off], inc[n]);
 }
 
 // advance the device step counter by `by` (after a two-step pair)

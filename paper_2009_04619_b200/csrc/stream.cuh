@@ -75,7 +75,43 @@ struct StreamParams {
   // stored (user-supplied) eta: [nz][ny][pitch] fp32 or null
   const float* eta;
   double dt;                    // the fp32 dt, widened (A/B = 1 -+ eta dt in fp64)
+  // two steps through L2 (PAIR kernels): step-1 blocks read
+  // (gu, gup) and write `out`; step-2 blocks read (gu2, gup2) and write `out2`
+  // after waiting on the step-1 progress of their own and neighbouring tiles
+  const int* pair_groups;       // group g -> role (1, 2) << 16 | tile row
+  unsigned* prog;               // per tile: planes completed x consumer warps
+  const CUtensorMap* gu2;
+  const CUtensorMap* gup2;
+  void* out2;
+  int src_i, src_j, src_k;      // source cell (local z; src_k < 0: none)
+  const void* inc;              // source increments (T)
+  int64_t ninc;
+  const unsigned long long* dstep;
+  int pair_dbg;                 // timing probes only (WAVE25_PAIR_DBG): 1 = no waits, 2 = no publication,
+                                // 8 = per-block timeline records
+  int pair_pk;                  // step 1 publishes its progress every pair_pk planes (and at the end)
+  int64_t pair_dbg_off;         // timeline records (pair_dbg & 8) at prog + this, 6 u64 per block
 };
+
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_acqrel_cta_shared_add(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+               : "=r"(old)
+               : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 template <typename T> __device__ __forceinline__ const CoefT<T>& coef_of(const StreamParams& P);
 template <> __device__ __forceinline__ const CoefT<float>& coef_of<float>(const StreamParams& P) { return P.k; }
@@ -227,7 +263,7 @@ __device__ __noinline__ typename VecT<T>::V pml_row_eta(typename VecT<T>::V L, t
   return vmake<T>(res);
 }
 
-template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0, typename T = float>
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0, typename T = float, int PAIR = 0>
 __global__ void __maxnreg__((StreamCfg<TX, CW, TY, TYT, MINB, RA, T>::MAXR))
 k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1)
          const __grid_constant__ CUtensorMap tm_up,   // u^{n-1}, box (CW, TY, 1)
@@ -248,6 +284,9 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   uint64_t* empty_p = full_p + SP;
   T* stab = reinterpret_cast<T*>(smem_raw + C::TAB_OFF);
   const int TABN = P.w + 2;
+  // PAIR step 1: per-publication arrival counts of the consumer warps, in a ring
+  // of 16 (warps drift by at most ~10 planes: the 9-stage u ring couples them)
+  __shared__ unsigned s_arr[PAIR ? 16 : 1];
 
   // ---- work unit ---------------------------------------------------------
   int b = blockIdx.x, ri = 0;
@@ -256,10 +295,18 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   const Region& G = P.reg[ri];
   b -= G.blk0;
   const int ncol = G.ntx * G.nty;
-  const int zc = b / ncol;
+  int zc = b / ncol;
   const int rem = b - zc * ncol;
   int tyi, txi;
-  if (P.order <= 0) {
+  int role = 0;                          // PAIR: 1 = step 1, 2 = step 2
+  if (PAIR) {
+    // groups of one tile row each, in dependency order (S1 r+1 before S2 r)
+    const int g = blockIdx.x / G.ntx, code = P.pair_groups[g];
+    role = code >> 28;
+    zc = (code >> 16) & 0xfff;
+    tyi = code & 0xffff;
+    txi = blockIdx.x - g * G.ntx;
+  } else if (P.order <= 0) {
     tyi = rem / G.ntx;
     txi = rem - tyi * G.ntx;
   } else {                                 // groups of P.order x-tiles; inside a group y-major
@@ -273,8 +320,14 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   const int cxo = min(((cx0 % TX) + TX) % TX, TX - CW);   // its offset inside the TX-wide box
   const int bx0 = cx0 - cxo;                              // box origin (128-B aligned when possible)
   const int ty0 = G.y0 + tyi * TY;
-  const int zs = G.z0 + zc * P.cz;
-  const int ze = min(zs + P.cz, G.z1);
+  int zs = G.z0 + zc * P.cz;
+  int ze = min(zs + P.cz, G.z1);
+  // PAIR step 2: chunk k covers planes [k cz - 4, (k+1) cz - 4), so that it
+  // needs only step-1 chunks <= k (scheduled before it: no deadlock)
+  if (PAIR && role == 2) {
+    zs = max(zs - R, G.z0);
+    ze = ze >= G.z1 ? G.z1 : ze - R;
+  }
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
@@ -291,6 +344,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
     fence_mbar_init();
   }
   for (int i = tid; i < 3 * TABN; i += C::NT) stab[i] = static_cast<const T*>(P.tab)[i];
+  if (PAIR && tid < 16) s_arr[tid] = 0;
   __syncthreads();
 
   // ======================= producer warp =================================
@@ -298,12 +352,52 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
     if (RA > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
     if (wid != C::NWC || lane != 0) return;
     const uint64_t pol_u = P.upol ? policy_evict_normal() : policy_evict_last();  // u^n: halo re-reads
-    const uint64_t pol_s = policy_evict_first();   // u^{n-1}, vdt2: streamed once
-    const CUtensorMap* mu = P.gu ? P.gu : &tm_u;
-    const CUtensorMap* mup = P.gup ? P.gup : &tm_up;
+    // u^{n-1}, vdt2: streamed once -- except in a PAIR step-1 block, whose
+    // u^{n-1} (overwritten by u^{n+1}) and vdt2 lines step 2 reads again
+    // (evict_last here and on the u^{n+1} stores measured no different, §5h)
+    const uint64_t pol_s = (PAIR && role == 1) ? policy_evict_normal() : policy_evict_first();
+    const CUtensorMap* mu = (PAIR && role == 2) ? P.gu2 : (P.gu ? P.gu : &tm_u);
+    const CUtensorMap* mup = (PAIR && role == 2) ? P.gup2 : (P.gup ? P.gup : &tm_up);
     const CUtensorMap* mv = P.gv ? P.gv : &tm_v;
+    // PAIR step 2: u^{n+1} plane p may be loaded once the step-1 blocks of this
+    // tile and of its x/y neighbours have stored it (release/acquire on the
+    // progress counters, then a generic->async proxy fence for the TMA read)
+    // counters: prog[k * ntile + tile] = planes of step-1 chunk k stored for the
+    // tile.  Neighbour counters (absent neighbours read the tile's own) are polled
+    // together; `known` = their minimum at the last poll of chunk kcur, so most
+    // planes need no poll at all
+    const int tile = tyi * G.ntx + txi, ntile = G.ntx * G.nty;
+    const int nbt[5] = {tile, txi > 0 ? tile - 1 : tile, txi + 1 < G.ntx ? tile + 1 : tile,
+                        tyi > 0 ? tile - G.ntx : tile, tyi + 1 < G.nty ? tile + G.ntx : tile};
+    unsigned known = 0;
+    int kcur = -1;
+    unsigned long long dbg_t0 = 0, dbg_slack = 0;
+    unsigned dbg_polls = 0, dbg_fails = 0;
+    if (PAIR && (P.pair_dbg & 8)) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
+    auto wait_plane = [&](int p) {
+      if (!PAIR || role != 2 || p < 0 || p >= P.nzl || (P.pair_dbg & 1)) return;
+      const int kp = p / P.cz;
+      const unsigned need = (unsigned)(p - kp * P.cz + 1);
+      if (kp != kcur) { kcur = kp; known = 0; }
+      if (known >= need) return;
+      const unsigned* base = P.prog + (int64_t)kp * ntile;
+      unsigned long long spins = 0;
+#pragma unroll 1
+      while (true) {
+        unsigned v[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) v[k] = ld_acquire_gpu_u32(base + nbt[k]);
+        known = min(min(min(v[0], v[1]), min(v[2], v[3])), v[4]);
+        if (P.pair_dbg & 8) { ++dbg_polls; if (known < need) ++dbg_fails; else dbg_slack += known - need; }
+        if (known >= need) break;
+        __nanosleep(32);
+        if (++spins > (1ull << 27)) __trap();       // a missing producer: fail, never hang
+      }
+      fence_proxy_async_global();
+    };
     // u plane p (local z, p >= zs-4) lives in u stage (p - zs + 4) % 9, use (p - zs + 4) / 9
     auto issue_u = [&](int p, int st) {
+      wait_plane(p);
       mbar_arrive_expect_tx(&full_u[st], C::U_STAGE * sizeof(T));
 #pragma unroll
       for (int h = 0; h < C::NH; ++h)
@@ -347,6 +441,19 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
           tma_prefetch_3d(mv, cx0, ty0, pp);
         }
       }
+    }
+    if (PAIR && (P.pair_dbg & 8)) {          // timeline record after the counters (timing probe)
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      unsigned long long* rec = reinterpret_cast<unsigned long long*>(P.prog + P.pair_dbg_off) + 6 * blockIdx.x;
+      rec[0] = ((unsigned long long)role << 48) | ((unsigned long long)zc << 32) | ((unsigned)tyi << 16) | txi;
+      rec[1] = smid;
+      rec[2] = dbg_t0;
+      rec[3] = t1;
+      rec[4] = ((unsigned long long)dbg_polls << 32) | dbg_fails;
+      rec[5] = dbg_slack;
     }
     return;
   }
@@ -435,7 +542,19 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
       Bc[c] = stab[2 * TABN + dx];
     }
   }
-  T* optr = static_cast<T*>(P.out) + (int64_t)(zs + R) * P.plane + (int64_t)gy * P.pitch + gx;
+  T* optr = static_cast<T*>((PAIR && role == 2) ? P.out2 : P.out) + (int64_t)(zs + R) * P.plane +
+            (int64_t)gy * P.pitch + gx;
+  // PAIR: the source cell is injected by the block that computes it (step 1
+  // adds inc[n], step 2 inc[n+1]); -1 if not in my vector rows
+  int src_r = -1, src_c = 0;
+  if (PAIR && P.src_k >= 0) {
+#pragma unroll
+    for (int r = 0; r < TYT; ++r)
+      if (gy + r == P.src_j && P.src_i >= gx && P.src_i < gx + NV && ((mask >> (r * NV + P.src_i - gx)) & 1u)) {
+        src_r = r;
+        src_c = P.src_i - gx;
+      }
+  }
 
   // ---- warm-up: planes zs-4 .. zs+3 (stages 0..7, first use) -> queue ----
   V q[9][TYT];
@@ -624,9 +743,29 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
                                    kg, PG, stab);
         }
       }
-      if (full) {
+      if (PAIR && src_r >= 0 && z == P.src_k) {
+        const unsigned long long n = *P.dstep + (unsigned long long)(role - 1);
+        if (n < (unsigned long long)P.ninc) {
 #pragma unroll
-        for (int r = 0; r < TYT; ++r) st_cs_v(optr + r * P.pitch, res[r]);
+          for (int r = 0; r < TYT; ++r)
+            if (r == src_r) {
+              T o[NV];
+#pragma unroll
+              for (int c = 0; c < NV; ++c) o[c] = vget(res[r], c);
+              o[src_c] = add_rn(o[src_c], static_cast<const T*>(P.inc)[n]);
+              res[r] = vmake<T>(o);
+            }
+        }
+      }
+      if (full) {
+        if (PAIR && role == 1) {
+          // u^{n+1} is re-read from L2 by the step-2 blocks: normal (not evict-first) stores
+#pragma unroll
+          for (int r = 0; r < TYT; ++r) *reinterpret_cast<V*>(optr + r * P.pitch) = res[r];
+        } else {
+#pragma unroll
+          for (int r = 0; r < TYT; ++r) st_cs_v(optr + r * P.pitch, res[r]);
+        }
       } else {
 #pragma unroll
         for (int r = 0; r < TYT; ++r)
@@ -650,6 +789,26 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
 #pragma unroll
             for (int c = 0; c < NV; ++c)
               if (mask & (1u << (r * NV + c))) rp[r * P.pitch + c] = vget(res[r], c);
+        }
+      }
+      if (PAIR && role == 1) {
+        // publish planes ..z (every pair_pk planes and at the end) once every
+        // consumer warp has stored its part: each warp arrives on the
+        // publication's slot (acq_rel, CTA scope); the last one adds the planes
+        // to the tile's counter with a gpu-scope release, which (cumulative)
+        // covers all the warps' stores.  Publications complete in order, so the
+        // counter = the number of finished planes.  (One gpu-scope release per
+        // plane costs ~1 us of store drain each: amortised over pair_pk planes.)
+        const int zr = z - zs;
+        if (zr % P.pair_pk == P.pair_pk - 1 || z == ze - 1) {
+          __syncwarp();
+          if (lane == 0 && !(P.pair_dbg & 2)) {
+            const unsigned e = (unsigned)(zr / P.pair_pk);
+            const unsigned old = atom_acqrel_cta_shared_add(&s_arr[e & 15], 1u);
+            if (old == ((e >> 4) + 1) * (unsigned)C::NWC - 1u)
+              red_release_gpu_add(P.prog + (int64_t)zc * G.ntx * G.nty + tyi * G.ntx + txi,
+                                  (unsigned)(zr - (int)e * P.pair_pk + 1));
+          }
         }
       }
       optr += P.plane;

@@ -64,11 +64,12 @@ struct KInfo {
   const char* name;
 };
 
-template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0, typename T = float>
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0, typename T = float, int PAIR = 0>
 static KInfo kinfo(const char* name) {
   using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T>;
   // tx = width of the u TMA box minus its halo (the half width for split boxes)
-  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA, T>, C::HW, CW, TY, C::NT, &C::smem_bytes, name};
+  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR>, C::HW, CW, TY, C::NT, &C::smem_bytes,
+               name};
 }
 
 // interior-kernel variants (WAVE25_INNER_TILE selects one; default first)
@@ -142,7 +143,9 @@ static KInfo pick(const KInfo* v, int n, const char* env) {
 }
 
 // KI_WALLX_E / KI_WALLY_E: the wall kernels of the stored-eta mode
-enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_WALLX_E = 4, KI_WALLY_E = 5, KI_N = 6 };
+// KI_PAIR: the two-step-through-L2 interior kernel
+enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_WALLX_E = 4, KI_WALLY_E = 5, KI_PAIR = 6,
+       KI_N = 7 };
 static bool is_wall(int ki) { return ki == KI_WALLX || ki == KI_WALLY || ki == KI_WALLX_E || ki == KI_WALLY_E; }
 
 static KInfo g_k[2][KI_N];   // [precision: 0 fp32, 1 fp64][kernel kind]
@@ -174,6 +177,8 @@ static void init_kernels() {
   g_k[0][KI_WALLY_E] = kinfo<64, 64, 8, 1, MODE_WALL_ETA, 3>("ey64x8x1m3");
   g_k[1][KI_WALLX_E] = kinfo<24, 16, 32, 1, MODE_WALL_ETA, 1, 0, double>("edx24c16x32x1");
   g_k[1][KI_WALLY_E] = kinfo<32, 32, 8, 1, MODE_WALL_ETA, 3, 0, double>("edy32x8x1m3");
+  g_k[0][KI_PAIR] = kinfo<248, 248, 8, 1, MODE_INNER, 1, 112, float, 1>("pair248x8x1r");
+  g_k[1][KI_PAIR] = kinfo<124, 124, 8, 1, MODE_INNER, 1, 112, double, 1>("dpair124x8x1r");
   g_k[1][KI_FUSED] = kinfo<64, 64, 8, 1, MODE_FUSED, 2, 0, double>("dfused64x8x1");
   done = true;
 }
@@ -254,7 +259,7 @@ struct wave_plan {
   Stats* stats_d = nullptr;
   // launch plans
   Maps maps[KI_N];
-  int occ[KI_N] = {1, 1, 1, 1, 1, 1};
+  int occ[KI_N] = {1, 1, 1, 1, 1, 1, 1};
   bool fused = false;                // WAVE25_FUSED=1: one launch, per-warp paths (measured slower)
   int pf = 1;                        // L2 prefetch distance (WAVE25_PF), measured best
   int prio_lo = 0, prio_hi = 0;      // stream priority range (launch attribute)
@@ -288,6 +293,16 @@ struct wave_plan {
   int t2_nblk = 0;
   std::vector<Launch> wall_p1, wall_p2;  // walls: u^{n+1} on the (w+8)-frame, u^{n+2} on the (w+4)-frame
   cudaGraphExec_t gexec2[16] = {};   // 1-pair graphs keyed by (cur, prv)
+  // two steps through L2 (WAVE_KERNEL_PAIR)
+  bool pair_ok = false;
+  Launch pair_launch;
+  int* pair_groups_d = nullptr;
+  int pair_dbg = 0;                  // WAVE25_PAIR_DBG timing probes (results invalid when set)
+  int pair_pk = 16;                  // WAVE25_PAIR_PK: planes per step-1 progress publication
+  int pair_cz = 256;                 // WAVE25_PAIR_CZ: z chunk of the pair kernel's blocks
+  unsigned* prog_d = nullptr;
+  int64_t prog_n = 0;
+  cudaGraphExec_t gexecP[16] = {};
   // fused peer-store halo exchange
   bool have_peers = false;
   wave_peers peers{};
@@ -375,7 +390,10 @@ static wave_status validate(const wave_desc* d) {
     return fail(WAVE_ERR_CONFIG, "unknown precision %d", d->precision);
   if (d->precision == WAVE_PREC_FP64 && d->kernel == WAVE_KERNEL_TB2)
     return fail(WAVE_ERR_CONFIG, "two-step blocking (TB2) is fp32 only");
-  if (d->kernel != WAVE_KERNEL_STREAM && d->kernel != WAVE_KERNEL_NAIVE && d->kernel != WAVE_KERNEL_TB2)
+  if (d->kernel == WAVE_KERNEL_PAIR && d->nz != d->nz_global)
+    return fail(WAVE_ERR_CONFIG, "the two-step (PAIR) kernel needs a single-slab plan");
+  if (d->kernel != WAVE_KERNEL_STREAM && d->kernel != WAVE_KERNEL_NAIVE && d->kernel != WAVE_KERNEL_TB2 &&
+      d->kernel != WAVE_KERNEL_PAIR)
     return fail(WAVE_ERR_CONFIG, "unknown kernel %d", d->kernel);
   if (d->dt == 0.f && (d->nz != d->nz_global)) return fail(WAVE_ERR_CONFIG, "auto dt needs a single-slab plan");
   return WAVE_OK;
@@ -518,6 +536,48 @@ static wave_status build_launches(wave_plan* P) {
   }
   // two-step temporal blocking: interior launch over the (w+4)-shrunk inner xy
   // box, walls in two single-step phases over frames of width w+8 and w+4
+  // two steps through L2: one launch over the inner xy footprint x all z,
+  // whole-z columns, 2 blocks per tile (step 1, step 2) in dependency order
+  P->pair_ok = false;
+  if (P->d.kernel == WAVE_KERNEL_PAIR && P->d.nz == P->d.nz_global && !P->eta_on && nx > 2 * w && ny > 2 * w) {
+    std::vector<Launch> tmp;
+    add_regions(P, KI_PAIR, {{w, nx - w, w, ny - w}}, all, &tmp);
+    if (tmp.size() == 1 && tmp[0].p.nreg == 1 && tmp[0].p.reg[0].nty < 65536 && (nz + 7) / 8 < 4096) {
+      Launch L = tmp[0];
+      Region& g = L.p.reg[0];
+      // z chunks of pair_cz planes (>= 8): short blocks keep step 2 close behind
+      // step 1 in time, so u^{n+1}, u^n and vdt2 are still in L2 when it reads them
+      const int cz = std::max(8, std::min(P->pair_cz, nz));
+      const int nzc = (nz + cz - 1) / cz;
+      L.p.cz = cz;
+      g.nzc = nzc;
+      g.blk0 = 0;
+      const int nrow = g.nty;
+      std::vector<int> groups;              // role << 28 | chunk << 16 | tile row, dependency order
+      for (int k = 0; k < nzc; ++k) {
+        groups.push_back((1 << 28) | (k << 16) | 0);
+        for (int r = 0; r < nrow; ++r) {
+          if (r + 1 < nrow) groups.push_back((1 << 28) | (k << 16) | (r + 1));
+          groups.push_back((2 << 28) | (k << 16) | r);
+        }
+      }
+      L.nblk = (int)groups.size() * g.ntx;
+      L.p.pf = 0;
+      const int64_t ntile = (int64_t)g.ntx * g.nty * nzc;
+      if (P->pair_groups_d) { cudaFree(P->pair_groups_d); P->pair_groups_d = nullptr; }
+      if (P->prog_d) { cudaFree(P->prog_d); P->prog_d = nullptr; }
+      CK(cudaMalloc(&P->pair_groups_d, groups.size() * sizeof(int)));
+      CK(cudaMemcpy(P->pair_groups_d, groups.data(), groups.size() * sizeof(int), cudaMemcpyHostToDevice));
+      const int64_t ndbg = (P->pair_dbg & 8) ? 12 * (int64_t)L.nblk + 2 : 0;   // u32 words, u64-aligned
+      L.p.pair_dbg_off = (ntile + 1) & ~(int64_t)1;
+      CK(cudaMalloc(&P->prog_d, (L.p.pair_dbg_off + ndbg) * sizeof(unsigned)));
+      P->prog_n = ntile;
+      L.p.pair_groups = P->pair_groups_d;
+      L.p.prog = P->prog_d;
+      P->pair_launch = L;
+      P->pair_ok = true;
+    }
+  }
   P->wall_p1.clear();
   P->wall_p2.clear();
   P->t2_ok = false;
@@ -919,13 +979,13 @@ static wave_status enqueue_pair(wave_plan* P, int cur, int prv, cudaStream_t s) 
     CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
     for (const Launch& L : P->wall_p1) CKST(launch_stream(P, L, cur, prv, P->buf[c], P->side));
     if (sp1) {
-      k_source_at<<<1, 1, 0, P->side>>>(P->buf[c], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+      k_source_at<float><<<1, 1, 0, P->side>>>(P->buf[c], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
                                         P->dstep, 0);
       CK(cudaGetLastError());
     }
     for (const Launch& L : P->wall_p2) CKST(launch_stream(P, L, c, cur, P->buf[d], P->side));
     if (sp2) {
-      k_source_at<<<1, 1, 0, P->side>>>(P->buf[d], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+      k_source_at<float><<<1, 1, 0, P->side>>>(P->buf[d], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
                                         P->dstep, 1);
       CK(cudaGetLastError());
     }
@@ -956,10 +1016,91 @@ static int pair_launches(const wave_plan* P) {
          (src && source_in_frame(P, 4)) + src;
 }
 
+// ---------------------------------------------------------------------------
+// two steps through L2 (WAVE_KERNEL_PAIR)
+// ---------------------------------------------------------------------------
+static bool pair_active(const wave_plan* P) {
+  return P->d.kernel == WAVE_KERNEL_PAIR && P->pair_ok && !P->eta_on && P->maps_g;
+}
+
+// source inside the PML walls: buf[b] += inc[n + delta] after the wall kernels
+// of step n + delta + 1 (the pair kernel injects an interior source itself)
+static wave_status pair_wall_source(wave_plan* P, int b, int delta, cudaStream_t s) {
+  if (!source_active(P) || !source_in_frame(P, 0)) return WAVE_OK;
+  if (P->d.precision == WAVE_PREC_FP64)
+    k_source_at<double><<<1, 1, 0, s>>>(reinterpret_cast<double*>(P->buf[b]), source_offset(P),
+                                        static_cast<const double*>(P->inc_d), P->ninc, P->dstep, delta);
+  else
+    k_source_at<float><<<1, 1, 0, s>>>(P->buf[b], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+                                       P->dstep, delta);
+  CK(cudaGetLastError());
+  return WAVE_OK;
+}
+
+static wave_status launch_pair_kernel(wave_plan* P, int cur, int prv, cudaStream_t s) {
+  const Launch& Lc = P->pair_launch;
+  StreamParams p = Lc.p;
+  p.gu = &P->maps_g[KI_PAIR].u[cur];        // step 1: u^n = A, u^{n-1} = B -> B
+  p.gup = &P->maps_g[KI_PAIR].up[prv];
+  p.gv = &P->maps_g[KI_PAIR].v;
+  p.out = P->buf[prv];
+  p.gu2 = &P->maps_g[KI_PAIR].u[prv];       // step 2: u^{n+1} = B, u^n = A -> A
+  p.gup2 = &P->maps_g[KI_PAIR].up[cur];
+  p.out2 = P->buf[cur];
+  p.rlo = p.rhi = nullptr;
+  // a source in the PML walls is added after the wall launches (pair_wall_source)
+  const bool src = source_active(P) && !source_in_frame(P, 0);
+  p.src_i = (int)P->si;
+  p.src_j = (int)P->sj;
+  p.src_k = src ? (int)(P->sk - P->d.z_offset) : -1;
+  p.inc = P->inc_d;
+  p.ninc = P->ninc;
+  p.dstep = P->dstep;
+  p.pair_dbg = P->pair_dbg;
+  p.pair_pk = P->pair_pk;
+  const Maps& M = P->maps[KI_PAIR];
+  void* args[] = {(void*)&M.u[cur], (void*)&M.up[prv], (void*)&M.v, (void*)&p};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(Lc.nblk);
+  cfg.blockDim = dim3(kernel_threads(P, KI_PAIR));
+  cfg.dynamicSmemBytes = kernel_smem(P, KI_PAIR);
+  cfg.stream = s;
+  CK(cudaLaunchKernelExC(&cfg, kernel_ptr(P, KI_PAIR), args));
+  return WAVE_OK;
+}
+
+// One pair: walls step 1 (u^{n+1} on the walls, into B), the interior pair
+// kernel (u^{n+1} into B, then u^{n+2} into A, read back through L2), walls
+// step 2 (u^{n+2} on the walls, into A).  In place: (cur, prv) unchanged.
+static wave_status enqueue_pair_l2(wave_plan* P, int cur, int prv, cudaStream_t s) {
+  CK(cudaMemsetAsync(P->prog_d, 0, P->prog_n * sizeof(unsigned), s));
+  for (const Launch& L : P->launches[0])
+    if (is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+  CKST(pair_wall_source(P, prv, 0, s));
+  CKST(launch_pair_kernel(P, cur, prv, s));
+  for (const Launch& L : P->launches[0])
+    if (is_wall(L.ki)) CKST(launch_stream(P, L, prv, cur, P->buf[cur], s));
+  CKST(pair_wall_source(P, cur, 1, s));
+  if (source_active(P)) {
+    k_advance<<<1, 1, 0, s>>>(P->dstep, 2);
+    CK(cudaGetLastError());
+  }
+  return WAVE_OK;
+}
+
+static wave_status one_pair_l2(wave_plan* P, int cur, int prv) { return enqueue_pair_l2(P, cur, prv, P->cap); }
+
+static int pair_l2_launches(const wave_plan* P) {
+  int n = 1 + (source_active(P) ? (source_in_frame(P, 0) ? 3 : 1) : 0);
+  for (const Launch& L : P->launches[0]) n += is_wall(L.ki) ? 2 : 0;
+  return n;
+}
+
 static void drop_graphs(wave_plan* P) {
   for (int i = 0; i < 16; ++i) {
     if (P->gexec[i]) { cudaGraphExecDestroy(P->gexec[i]); P->gexec[i] = nullptr; }
     if (P->gexec2[i]) { cudaGraphExecDestroy(P->gexec2[i]); P->gexec2[i] = nullptr; }
+    if (P->gexecP[i]) { cudaGraphExecDestroy(P->gexecP[i]); P->gexecP[i] = nullptr; }
   }
   for (int i = 0; i < 2; ++i)
     if (P->gexec_peer[i]) { cudaGraphExecDestroy(P->gexec_peer[i]); P->gexec_peer[i] = nullptr; }
@@ -1056,6 +1197,9 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
     for (const void* f : aux) cudaFuncGetAttributes(&fa, f);
   }
   if (const char* e = getenv("WAVE25_PF")) P->pf = atoi(e);
+  if (const char* e = getenv("WAVE25_PAIR_DBG")) P->pair_dbg = atoi(e);
+  if (const char* e = getenv("WAVE25_PAIR_PK")) P->pair_pk = std::max(1, atoi(e));
+  if (const char* e = getenv("WAVE25_PAIR_CZ")) P->pair_cz = std::max(8, atoi(e));
   if (const char* e = getenv("WAVE25_WALL_PRIO")) P->wall_prio = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_SERIAL")) P->serial = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_XFUSE")) P->xfuse = atoi(e) != 0;
@@ -1111,7 +1255,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, P->t2.fn, P->t2.nt, sm);
     if (occ < 1) return bail(fail(WAVE_ERR_CONFIG, "two-step kernel does not fit on an SM (w = %d)", P->d.pml_width));
     P->occ_t2 = occ;
-    for (const void* f : {(const void*)k_source_at, (const void*)k_advance}) cudaFuncGetAttributes(&fa, f);
+    for (const void* f : {(const void*)k_source_at<float>, (const void*)k_source_at<double>, (const void*)k_advance}) cudaFuncGetAttributes(&fa, f);
   }
   *out = P;
   return WAVE_OK;
@@ -1122,6 +1266,19 @@ void wave_plan_destroy(wave_plan* P) {
   drop_graphs(P);
   if (P->tab_d) cudaFree(P->tab_d);
   if (P->maps_g) cudaFree(P->maps_g);
+  if (P->prog_d && (P->pair_dbg & 8) && P->pair_ok) {   // timing probe: dump the last launch's timeline
+    const int n = P->pair_launch.nblk;
+    std::vector<unsigned long long> h(6 * (size_t)n);
+    cudaMemcpy(h.data(), P->prog_d + P->pair_launch.p.pair_dbg_off, h.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen("pair_timeline.txt", "w")) {
+      for (int i = 0; i < n; ++i)
+        fprintf(f, "%d %llu %llu %llu %llu %llu %llu %llu\n", i, h[6 * i] >> 48, (h[6 * i] >> 32) & 0xffff,
+                (h[6 * i] >> 16) & 0xffff, h[6 * i + 1], h[6 * i + 2], h[6 * i + 3], h[6 * i + 4] >> 32);
+      fclose(f);
+    }
+  }
+  if (P->pair_groups_d) cudaFree(P->pair_groups_d);
+  if (P->prog_d) cudaFree(P->prog_d);
   if (P->dstep) cudaFree(P->dstep);
   if (P->stats_d) cudaFree(P->stats_d);
   if (P->ddone) cudaFree(P->ddone);
@@ -1343,7 +1500,15 @@ wave_status wave_step(wave_plan* P, int64_t nsteps, void* stream) {
   if (P->d.nz != P->d.nz_global) return fail(WAVE_ERR_STATE, "multi-slab plan: use the split-step calls");
   cudaStream_t s = (cudaStream_t)stream;
   int64_t left = nsteps;
-  if (left >= 2 && tb2_active(P)) {
+  if (left >= 2 && pair_active(P)) {
+    cudaGraphExec_t* g = &P->gexecP[P->cur * 4 + P->prv];
+    if (!*g) CKST(capture(P, g, one_pair_l2, P->cur, P->prv));
+    while (left >= 2) {                // in place: the state does not change
+      CK(cudaGraphLaunch(*g, s));
+      left -= 2;
+      P->step += 2;
+    }
+  } else if (left >= 2 && tb2_active(P)) {
     while (left >= 2) {                // one graph per (cur, prv) state; a pair moves to (D, C)
       CKST(ensure_pair_graph(P, P->cur, P->prv));
       CK(cudaGraphLaunch(P->gexec2[P->cur * 4 + P->prv], s));
@@ -1584,7 +1749,8 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
   if (nsteps < 0) return fail(WAVE_ERR_CONFIG, "nsteps < 0");
   if (P->d.nz != P->d.nz_global) return fail(WAVE_ERR_STATE, "multi-slab plan: use the split-step calls");
   if (P->d.kernel == WAVE_KERNEL_NAIVE) return fail(WAVE_ERR_STATE, "profiling needs the stream kernels");
-  const bool pairs = tb2_active(P);
+  const bool pairl2 = pair_active(P);
+  const bool pairs = tb2_active(P) || pairl2;
   if (pairs && nsteps % 2) return fail(WAVE_ERR_CONFIG, "two-step plans profile an even number of steps");
   cudaStream_t s = (cudaStream_t)stream;
   struct Rec { int kind; cudaEvent_t a, b; };
@@ -1601,6 +1767,41 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
   // every launch serialized on `stream` so every event pair brackets one kernel alone
   for (int64_t n = 0; n < nsteps; n += pairs ? 2 : 1) {
     const int cur = P->cur, prv = P->prv;
+    if (pairl2) {
+      CK(cudaMemsetAsync(P->prog_d, 0, P->prog_n * sizeof(unsigned), s));
+      for (const Launch& L : P->launches[0])
+        if (is_wall(L.ki)) {
+          CKST(mk(kk_of(L.ki), s));
+          CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+          CK(cudaEventRecord(recs.back().b, s));
+        }
+      if (src && source_in_frame(P, 0)) {
+        CKST(mk(WAVE_KK_SOURCE, s));
+        CKST(pair_wall_source(P, prv, 0, s));
+        CK(cudaEventRecord(recs.back().b, s));
+      }
+      CKST(mk(WAVE_KK_INTERIOR, s));
+      CKST(launch_pair_kernel(P, cur, prv, s));
+      CK(cudaEventRecord(recs.back().b, s));
+      for (const Launch& L : P->launches[0])
+        if (is_wall(L.ki)) {
+          CKST(mk(kk_of(L.ki), s));
+          CKST(launch_stream(P, L, prv, cur, P->buf[cur], s));
+          CK(cudaEventRecord(recs.back().b, s));
+        }
+      if (src && source_in_frame(P, 0)) {
+        CKST(mk(WAVE_KK_SOURCE, s));
+        CKST(pair_wall_source(P, cur, 1, s));
+        CK(cudaEventRecord(recs.back().b, s));
+      }
+      if (src) {
+        CKST(mk(WAVE_KK_SOURCE, s));
+        k_advance<<<1, 1, 0, s>>>(P->dstep, 2);
+        CK(cudaEventRecord(recs.back().b, s));
+      }
+      P->step += 2;
+      continue;
+    }
     if (pairs) {
       int c, d;
       pair_targets(cur, prv, &c, &d);
@@ -1611,7 +1812,7 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
       }
       if (src && source_in_frame(P, 8)) {
         CKST(mk(WAVE_KK_SOURCE, s));
-        k_source_at<<<1, 1, 0, s>>>(P->buf[c], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+        k_source_at<float><<<1, 1, 0, s>>>(P->buf[c], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
                                     P->dstep, 0);
         CK(cudaEventRecord(recs.back().b, s));
       }
@@ -1622,7 +1823,7 @@ wave_status wave_step_profiled(wave_plan* P, int64_t nsteps, void* stream, doubl
       }
       if (src && source_in_frame(P, 4)) {
         CKST(mk(WAVE_KK_SOURCE, s));
-        k_source_at<<<1, 1, 0, s>>>(P->buf[d], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
+        k_source_at<float><<<1, 1, 0, s>>>(P->buf[d], source_offset(P), static_cast<const float*>(P->inc_d), P->ninc,
                                     P->dstep, 1);
         CK(cudaEventRecord(recs.back().b, s));
       }
@@ -1683,13 +1884,14 @@ int32_t wave_launches_per_step(const wave_plan* P) {
 int64_t wave_launches(const wave_plan* P, int64_t nsteps) {
   if (!P || nsteps < 0) return -1;
   const int64_t single = wave_launches_per_step(P);
+  if (pair_active(P)) return (nsteps / 2) * pair_l2_launches(P) + (nsteps % 2) * single;
   if (!tb2_active(P)) return single * nsteps;
   return (nsteps / 2) * pair_launches(P) + (nsteps % 2) * single;
 }
 
 int32_t wave_steps_per_launch(const wave_plan* P) {
   if (!P) return -1;
-  return tb2_active(P) ? 2 : 1;
+  return (tb2_active(P) || pair_active(P)) ? 2 : 1;
 }
 
 wave_status wave_plan_bind_eta(wave_plan* P, float* eta_buf, void* stream) {

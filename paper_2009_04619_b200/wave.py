@@ -53,7 +53,7 @@ class WavePlan:
                  nz_global=None, z_offset=0, device=None, stream=None, precision="fp32"):
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         kern = {"stream": _abi.WAVE_KERNEL_STREAM, "naive": _abi.WAVE_KERNEL_NAIVE,
-                "tb2": _abi.WAVE_KERNEL_TB2}[kernel]
+                "tb2": _abi.WAVE_KERNEL_TB2, "pair": _abi.WAVE_KERNEL_PAIR}[kernel]
         prec = {"fp32": _abi.WAVE_PREC_FP32, "fp64": _abi.WAVE_PREC_FP64}[precision]
         self.dtype = torch.float64 if prec == _abi.WAVE_PREC_FP64 else torch.float32
         self.desc = _abi.make_desc(nx, ny, nz, w, h, float(np.float32(dt)), eta_max, kern,
