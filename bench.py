@@ -419,6 +419,8 @@ def run_ours(args, rank, world, local):
                         "note": "value is the first timed run (driver contract); repeats follow PAPER.md L885-888"},
         }
         print(json.dumps(line), flush=True)
+    if hasattr(runner, "close"):
+        runner.close()                 # unmap the neighbours' buffers (collective)
     plan.close()
     if dist is not None:
         dist.destroy_process_group()

@@ -290,8 +290,26 @@ typedef struct {
 } wave_peers;
 
 /* Install (or clear, with NULL) the neighbour wiring.  Resets the step
- * counters used by the flag protocol. */
+ * counters used by the flag protocol.  A neighbour pointer that lives on
+ * another device needs peer access from the plan's device: it is enabled here
+ * (cudaDeviceEnablePeerAccess); CUDA error if the two devices cannot access
+ * each other (no NVLink/PCIe P2P path). */
 WAVE_API wave_status wave_set_peers(wave_plan *plan, const wave_peers *peers);
+
+/* Cross-process mapping of device buffers for the peer wiring (CUDA IPC; the
+ * current device is the caller's).
+ *   wave_ipc_export: handle (64 bytes, cudaIpcMemHandle_t) of the allocation
+ *     holding dptr and dptr's byte offset inside it (dptr may be an interior
+ *     pointer of a caching-allocator block).
+ *   wave_ipc_import: opens a handle exported by ANOTHER process on the current
+ *     device with lazy peer access (the allocation may live on another GPU);
+ *     *base = the mapping (pass to wave_ipc_release), *dptr = base + offset.
+ *   wave_ipc_release: unmaps a base returned by wave_ipc_import.
+ * CUDA errors (e.g. a handle from the same process, VMM/expandable-segment
+ * memory) are returned as WAVE_ERR_CUDA with the driver's message. */
+WAVE_API wave_status wave_ipc_export(const void *dptr, void *handle64, int64_t *offset);
+WAVE_API wave_status wave_ipc_import(const void *handle64, int64_t offset, void **base, void **dptr);
+WAVE_API wave_status wave_ipc_release(void *base);
 
 /* Advance nsteps steps on a z-slab with the halo exchange fused into the
  * compute: every step (a) waits until both neighbours have completed the

@@ -30,6 +30,7 @@ EXPORTS = [
     "wave_step_index", "wave_get_dt", "wave_launches_per_step", "wave_kernel_points",
     "wave_step_profiled", "wave_set_peers", "wave_step_peer", "wave_push_halo",
     "wave_plan_bind_aux", "wave_launches", "wave_steps_per_launch", "wave_plan_bind_eta", "wave_set_eta",
+    "wave_ipc_export", "wave_ipc_import", "wave_ipc_release",
 ]
 KERNEL_KINDS = ["interior", "xwalls", "ywalls", "source"]
 
@@ -116,6 +117,9 @@ def lib() -> ctypes.CDLL:
                 "wave_steps_per_launch": ([P], i32),
                 "wave_plan_bind_eta": ([P, P, P], i32),
                 "wave_set_eta": ([P, P, i32, P], i32),
+                "wave_ipc_export": ([P, P, ctypes.POINTER(i64)], i32),
+                "wave_ipc_import": ([P, i64, ctypes.POINTER(P), ctypes.POINTER(P)], i32),
+                "wave_ipc_release": ([P], i32),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)
@@ -293,3 +297,24 @@ def wave_step_peer(plan, nsteps: int, stream: int) -> None:
 
 def wave_push_halo(plan, which: int, stream: int) -> None:
     check(lib().wave_push_halo(plan, int(which), stream))
+
+
+def wave_ipc_export(dptr: int) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding dptr, byte offset of dptr in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    check(lib().wave_ipc_export(ctypes.c_void_p(dptr), h, ctypes.byref(off)))
+    return h.raw, int(off.value)
+
+
+def wave_ipc_import(handle: bytes, offset: int) -> tuple[int, int]:
+    """Map another process's exported allocation on the current device: (base, dptr)."""
+    if len(handle) != 64:
+        raise ValueError("CUDA IPC handles are 64 bytes")
+    base, ptr = ctypes.c_void_p(), ctypes.c_void_p()
+    check(lib().wave_ipc_import(handle, int(offset), ctypes.byref(base), ctypes.byref(ptr)))
+    return int(base.value), int(ptr.value)
+
+
+def wave_ipc_release(base: int) -> None:
+    check(lib().wave_ipc_release(ctypes.c_void_p(base)))

@@ -1589,6 +1589,63 @@ static wave_status ensure_peer_graph(wave_plan* P, int par) {
   return WAVE_OK;
 }
 
+// peer access from the current device to the device owning p (no-op if same)
+static wave_status enable_peer_for(const void* p) {
+  if (!p) return WAVE_OK;
+  cudaPointerAttributes a{};
+  CK(cudaPointerGetAttributes(&a, p));
+  if (a.type != cudaMemoryTypeDevice) return fail(WAVE_ERR_CONFIG, "peer pointer is not device memory");
+  int me = 0;
+  CK(cudaGetDevice(&me));
+  if (a.device == me || a.device < 0) return WAVE_OK;
+  int can = 0;
+  CK(cudaDeviceCanAccessPeer(&can, me, a.device));
+  if (!can) return fail(WAVE_ERR_CUDA, "device %d cannot access peer device %d", me, a.device);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+  else if (e != cudaSuccess) return fail(WAVE_ERR_CUDA, "cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+  return WAVE_OK;
+}
+
+wave_status wave_ipc_export(const void* dptr, void* handle64, int64_t* offset) {
+  if (!dptr || !handle64 || !offset) return fail(WAVE_ERR_CONFIG, "null argument");
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(WAVE_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  const CUresult r = range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr));
+  if (r != CUDA_SUCCESS) return fail(WAVE_ERR_CUDA, "cuMemGetAddressRange failed (%d)", (int)r);
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, sizeof h);
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dptr) - base);
+  return WAVE_OK;
+}
+
+wave_status wave_ipc_import(const void* handle64, int64_t offset, void** base, void** dptr) {
+  if (!handle64 || !base || !dptr || offset < 0) return fail(WAVE_ERR_CONFIG, "bad argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  void* b = nullptr;
+  CK(cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess));
+  *base = b;
+  *dptr = static_cast<char*>(b) + offset;
+  return WAVE_OK;
+}
+
+wave_status wave_ipc_release(void* base) {
+  if (!base) return WAVE_OK;
+  CK(cudaIpcCloseMemHandle(base));
+  return WAVE_OK;
+}
+
 wave_status wave_set_peers(wave_plan* P, const wave_peers* peers) {
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "plan not bound");
   drop_graphs(P);
@@ -1606,6 +1663,9 @@ wave_status wave_set_peers(wave_plan* P, const wave_peers* peers) {
   if (lo && (P->d.z_offset == 0 || peers->lo_nz < R)) return fail(WAVE_ERR_CONFIG, "no lower neighbour at z_offset 0");
   if (hi && P->d.z_offset + P->d.nz >= P->d.nz_global) return fail(WAVE_ERR_CONFIG, "no upper neighbour at the top");
   if (P->d.kernel != WAVE_KERNEL_STREAM) return fail(WAVE_ERR_CONFIG, "peer stepping needs the stream kernels");
+  for (const void* q : {(const void*)peers->lo_buf[0], (const void*)peers->lo_buf[1], (const void*)peers->hi_buf[0],
+                        (const void*)peers->hi_buf[1], (const void*)peers->lo_flags, (const void*)peers->hi_flags})
+    CKST(enable_peer_for(q));
   if (!P->ddone) CK(cudaMalloc(&P->ddone, sizeof(unsigned long long)));
   CK(cudaMemset(P->ddone, 0, sizeof(unsigned long long)));
   P->peers = *peers;

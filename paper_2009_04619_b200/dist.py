@@ -4,8 +4,10 @@ which is single-GPU).
 Two exchange paths:
 
 * PeerSlabRunner (default): the exchange is fused into the compute.  Each
-  rank maps its neighbours' wavefield buffers and flag words (CUDA IPC over
-  NVLink / NVSwitch); the streaming kernels store the 4 edge planes of u_next
+  rank maps its neighbours' wavefield buffers and flag words (CUDA IPC handles
+  exported and opened by libwave25 on the rank's own device with lazy peer
+  access; wave_set_peers enables peer access over NVLink / NVSwitch); the
+  streaming kernels store the 4 edge planes of u_next
   straight into the neighbours' ghost planes as they compute them, and
   system-scope release/acquire step flags order consecutive steps
   (wave_step_peer).  torch.distributed is used only to swap the IPC handles
@@ -136,16 +138,32 @@ class SlabRunner:
             self.plan.step_finish()
 
 
-def _share(t: torch.Tensor):
-    """Picklable CUDA IPC description of a tensor (torch's own mechanism)."""
-    from torch.multiprocessing.reductions import reduce_tensor
-    fn, args = reduce_tensor(t)
-    return fn, args
+class _PeerBuf:
+    """A neighbour's device buffer mapped into this process (CUDA IPC, opened
+    on this rank's device with lazy peer access); quacks like a tensor for
+    WavePlan.set_peers (data_ptr())."""
+
+    def __init__(self, desc, device):
+        from . import _abi
+        handle, offset = desc
+        with torch.cuda.device(device):
+            self.base, self.ptr = _abi.wave_ipc_import(handle, offset)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def release(self) -> None:
+        from . import _abi
+        if self.base:
+            _abi.wave_ipc_release(self.base)
+            self.base = self.ptr = 0
 
 
-def _open(desc):
-    fn, args = desc
-    return fn(*args)
+def _export(t: torch.Tensor):
+    """(IPC handle, byte offset) of a CUDA tensor's memory."""
+    from . import _abi
+    with torch.cuda.device(t.device):
+        return _abi.wave_ipc_export(t.data_ptr())
 
 
 class PeerSlabRunner:
@@ -156,17 +174,31 @@ class PeerSlabRunner:
         self.plan, self.rank, self.world, self.group = plan, rank, world, group
         if not hasattr(plan, "flags"):
             plan.flags = torch.zeros(2, dtype=torch.int64, device=plan.device)
-        mine = (_share(plan.bufs[0]), _share(plan.bufs[1]), _share(plan.flags), plan.nz)
+        torch.cuda.synchronize(plan.device)
+        mine = (_export(plan.bufs[0]), _export(plan.bufs[1]), _export(plan.flags), plan.nz)
         allv = [None] * world
         dist.all_gather_object(allv, mine, group=group)
         lo = allv[rank - 1] if rank > 0 else None
         hi = allv[rank + 1] if rank < world - 1 else None
-        self._lo = (_open(lo[0]), _open(lo[1]), _open(lo[2]), lo[3]) if lo else None
-        self._hi = (_open(hi[0]), _open(hi[1]), _open(hi[2]), hi[3]) if hi else None
+        dev = plan.device
+        self._lo = (_PeerBuf(lo[0], dev), _PeerBuf(lo[1], dev), _PeerBuf(lo[2], dev), lo[3]) if lo else None
+        self._hi = (_PeerBuf(hi[0], dev), _PeerBuf(hi[1], dev), _PeerBuf(hi[2], dev), hi[3]) if hi else None
         plan.set_peers(lo_bufs=self._lo[:2] if self._lo else None, hi_bufs=self._hi[:2] if self._hi else None,
                        lo_nz=self._lo[3] if self._lo else 0, lo_flags=self._lo[2] if self._lo else None,
                        hi_flags=self._hi[2] if self._hi else None)
         self._barrier()
+
+    def close(self) -> None:
+        """Unwire the plan and unmap the neighbours' buffers (collective: every
+        rank calls it after its last step; the barrier keeps each mapping alive
+        until no rank can still be storing through it)."""
+        self._barrier()
+        self.plan.clear_peers()
+        for side in (self._lo, self._hi):
+            if side:
+                for b in side[:3]:
+                    b.release()
+        self._lo = self._hi = None
 
     def _barrier(self):
         torch.cuda.synchronize(self.plan.device)

@@ -132,7 +132,8 @@ class WavePlan:
     # ---- fused peer-store halo exchange ----------------------------------
     def set_peers(self, lo_bufs=None, hi_bufs=None, lo_nz: int = 0, lo_flags=None, hi_flags=None) -> None:
         """Wire the z-neighbours for step_peer: their two wavefield buffers and
-        flag words as torch tensors on any device (peer / IPC mappings); None
+        flag words (torch tensors, or anything with data_ptr() -- e.g. the
+        IPC mappings of dist.PeerSlabRunner -- on this or a peer device); None
         where there is no neighbour.  Allocates this plan's zeroed flag words."""
         if not hasattr(self, "flags"):
             self.flags = torch.zeros(2, dtype=torch.int64, device=self.device)
@@ -151,6 +152,12 @@ class WavePlan:
         torch.cuda.synchronize(self.device)
         with torch.cuda.device(self.device):
             _abi.wave_set_peers(self._plan, pe)
+
+    def clear_peers(self) -> None:
+        """Remove the neighbour wiring (before the neighbours' mappings go away)."""
+        with torch.cuda.device(self.device):
+            _abi.wave_set_peers(self._plan, None)
+        self._peer_refs = None
 
     def step_peer(self, n: int = 1, stream=None) -> None:
         with torch.cuda.device(self.device):

@@ -468,7 +468,7 @@ def _peer_worker(rank, world, port, steps, q):
         runner.step(steps)
         torch.cuda.synchronize()
         q.put((rank, p.read(0).cpu().numpy()))
-        dist.barrier()            # keep buffers mapped until every rank is done
+        runner.close()            # collective: keeps buffers mapped until every rank is done
         p.close()
     finally:
         dist.destroy_process_group()
@@ -577,3 +577,13 @@ def test_semi_stencil_shape_within_gate():
     out = subprocess.run([sys.executable, "-c", SEMI_SCRIPT, root], env={**base, "WAVE25_ABLATION": "semi_32x16"},
                          capture_output=True, text=True, check=True).stdout
     assert float(out.split()[-1]) <= TOL, out
+
+
+def test_ipc_export_offsets():
+    # wave_ipc_export: handle of the whole allocation + the byte offset of an
+    # interior pointer (what PeerSlabRunner ships to the neighbours)
+    from paper_2009_04619_b200 import _abi
+    t = torch.zeros(1 << 20, dtype=torch.float32, device="cuda")
+    h0, o0 = _abi.wave_ipc_export(t.data_ptr())
+    h1, o1 = _abi.wave_ipc_export(t[1000:].data_ptr())
+    assert len(h0) == 64 and h0 == h1 and o1 - o0 == 4000
