@@ -502,9 +502,15 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   // column-constant one (d_x eta only).  Precompute those coefficients once:
   //   cg = (eta(+e_a) - eta(-e_a)) / (2 h_a), A_d, B_d
   // Warps mixing both (corners) take the general path.
+  // The coefficients live in small per-CTA shared tables (cg, A, B per tile
+  // column / row), re-read inside the specialised branches each plane: kept in
+  // registers across the loop they were spilled to local memory around the
+  // general path's call, and the LDL latency stalled the wall kernels (§5).
   int wkind = 0;                             // 1: y-wall rows, 2: x-wall columns, 0: general
-  T cgr[TYT], Ar[TYT], Br[TYT];              // y-wall: per row
-  T cgc[NV], Ac[NV], Bc[NV];                 // x-wall: per column
+  constexpr bool WT = MODE == MODE_WALL || MODE == MODE_FUSED;
+  __shared__ __align__(16) T s_wc[WT ? 3 * CW : 1];   // per column: cg_x, A, B
+  __shared__ __align__(16) T s_wr[WT ? 3 * TY : 1];   // per row: cg_y, A, B
+  const int wci = min(NV * lx, CW - NV);     // my first table column (phantom lanes clamp)
   // fused mode: warps touching the x/y PML take the same specialised paths
   const bool wallw = MODE == MODE_WALL || MODE == MODE_WALL_ETA || (MODE == MODE_FUSED && warp_xy_pml);
   if (MODE == MODE_WALL || MODE == MODE_FUSED) {
@@ -523,24 +529,32 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
     // an inner point (d = 0) inside a wall region (the frames of a two-step
     // pair reach 4 or 8 cells into the inner box) takes cg = 0, A = B = 1:
     // ((2u - up) + v (L + 0)) / 1, bitwise the inner update (up to the sign of 0)
+    if (lx == 0) {                           // one writer per tile row
 #pragma unroll
-    for (int r = 0; r < TYT; ++r) {
-      const int dy = dist1(gy + r, P.ny, P.w);
-      cgr[r] = dy == 0 ? T(0)
-                       : mul_rn(sub_rn(stab[dist1(gy + r + 1, P.ny, P.w)], stab[dist1(gy + r - 1, P.ny, P.w)]),
-                                PG.i2hy);
-      Ar[r] = stab[TABN + dy];
-      Br[r] = stab[2 * TABN + dy];
+      for (int r = 0; r < TYT; ++r) {
+        const int dy = dist1(gy + r, P.ny, P.w);
+        s_wr[ly * TYT + r] =
+            dy == 0 ? T(0)
+                    : mul_rn(sub_rn(stab[dist1(gy + r + 1, P.ny, P.w)], stab[dist1(gy + r - 1, P.ny, P.w)]),
+                             PG.i2hy);
+        s_wr[TY + ly * TYT + r] = stab[TABN + dy];
+        s_wr[2 * TY + ly * TYT + r] = stab[2 * TABN + dy];
+      }
     }
+    if (ly == 0 && NV * lx < CW) {           // one writer per tile column
 #pragma unroll
-    for (int c = 0; c < NV; ++c) {
-      const int dx = dist1(gx + c, P.nx, P.w);
-      cgc[c] = dx == 0 ? T(0)
-                       : mul_rn(sub_rn(stab[dist1(gx + c + 1, P.nx, P.w)], stab[dist1(gx + c - 1, P.nx, P.w)]),
-                                PG.i2hx);
-      Ac[c] = stab[TABN + dx];
-      Bc[c] = stab[2 * TABN + dx];
+      for (int c = 0; c < NV; ++c) {
+        const int dx = dist1(gx + c, P.nx, P.w);
+        s_wc[NV * lx + c] =
+            dx == 0 ? T(0)
+                    : mul_rn(sub_rn(stab[dist1(gx + c + 1, P.nx, P.w)], stab[dist1(gx + c - 1, P.nx, P.w)]),
+                             PG.i2hx);
+        s_wc[CW + NV * lx + c] = stab[TABN + dx];
+        s_wc[2 * CW + NV * lx + c] = stab[2 * TABN + dx];
+      }
     }
+    // consumer warps only (the producer warps have left): named barrier 1
+    asm volatile("bar.sync 1, %0;" ::"r"(C::NWC * 32) : "memory");
   }
   T* optr = static_cast<T*>((PAIR && role == 2) ? P.out2 : P.out) + (int64_t)(zs + R) * P.plane +
             (int64_t)gy * P.pitch + gx;
@@ -716,16 +730,19 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
         for (int r = 0; r < TYT; ++r) {
           T o[NV];
           if (wkind == 1) {
+            const int ri = ly * TYT + r;
+            const T cg = s_wr[ri], Aw = s_wr[TY + ri], Bw = s_wr[2 * TY + ri];
 #pragma unroll
             for (int c = 0; c < NV; ++c) {
-              const T gya = mul_rn(cgr[r], mul_rn(sub_rn(vget(Y[R + r + 1], c), vget(Y[R + r - 1], c)), K.i2h[1]));
-              o[c] = upd_pml(L[r][c], gya, X[r][XC + c], vget(upv[r], c), vget(vv[r], c), Ar[r], Br[r]);
+              const T gya = mul_rn(cg, mul_rn(sub_rn(vget(Y[R + r + 1], c), vget(Y[R + r - 1], c)), K.i2h[1]));
+              o[c] = upd_pml(L[r][c], gya, X[r][XC + c], vget(upv[r], c), vget(vv[r], c), Aw, Bw);
             }
           } else {
+            const V cgv = ldv(s_wc + wci), Av = ldv(s_wc + CW + wci), Bv = ldv(s_wc + 2 * CW + wci);
 #pragma unroll
             for (int c = 0; c < NV; ++c) {
-              const T gxa = mul_rn(cgc[c], mul_rn(sub_rn(X[r][XC + c + 1], X[r][XC + c - 1]), K.i2h[0]));
-              o[c] = upd_pml(L[r][c], gxa, X[r][XC + c], vget(upv[r], c), vget(vv[r], c), Ac[c], Bc[c]);
+              const T gxa = mul_rn(vget(cgv, c), mul_rn(sub_rn(X[r][XC + c + 1], X[r][XC + c - 1]), K.i2h[0]));
+              o[c] = upd_pml(L[r][c], gxa, X[r][XC + c], vget(upv[r], c), vget(vv[r], c), vget(Av, c), vget(Bv, c));
             }
           }
           res[r] = vmake<T>(o);
