@@ -169,8 +169,15 @@ __global__ void k_vdt2(T* out, const float* V, int64_t pitch, int nx, int64_t ro
   const int nx4 = (nx + 3) / 4;
   for (int64_t row = blockIdx.x; row < rows; row += gridDim.x)
     for (int x4 = threadIdx.x; x4 < nx4; x4 += blockDim.x) {
-      const float4 v = *reinterpret_cast<const float4*>(V + row * pitch + 4 * x4);
-      const float vv[4] = {v.x, v.y, v.z, v.w};
+      // the row's last vector may reach into the (never written) pitch padding:
+      // load only the valid elements there
+      float vv[4] = {0.f, 0.f, 0.f, 0.f};
+      if (4 * x4 + 3 < nx) {
+        const float4 v = *reinterpret_cast<const float4*>(V + row * pitch + 4 * x4);
+        vv[0] = v.x; vv[1] = v.y; vv[2] = v.z; vv[3] = v.w;
+      } else {
+        for (int c = 0; 4 * x4 + c < nx; ++c) vv[c] = V[row * pitch + 4 * x4 + c];
+      }
       T o[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {

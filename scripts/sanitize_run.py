@@ -1,5 +1,5 @@
 """Small end-to-end runs for compute-sanitizer (development aid): every kernel
-family (stream / naive / tb2), fp32 and fp64, stored eta, the paper-shape
+family (stream / naive / tb2 / pair), fp32 and fp64, stored eta, the paper-shape
 ablation kernels, graph replay and the slab split path, on C1 / RAGGED-size
 grids."""
 import os, sys
@@ -26,7 +26,7 @@ def run(s, kernel="stream", precision="fp32", eta=False, steps=5):
 cases = [("C1", {}), ("RAGGED", {}), ("RAGGED", dict(nx=9, ny=11, nz=10, w=2, src=(4, 5, 5)))]
 for name, kw in cases:
     s = synth.scenario(name, **kw)
-    for kernel in ("stream", "naive", "tb2"):
+    for kernel in ("stream", "naive", "tb2", "pair"):
         run(s, kernel)
     run(s, "stream", "fp64")
     run(s, "naive", "fp64")
