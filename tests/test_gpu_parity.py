@@ -66,6 +66,18 @@ def test_c1_point_source(kernel):
     assert rel_linf(g, r) <= TOL and rel_linf(gp, rp) <= TOL
 
 
+def test_c2_full_run_vs_oracle():
+    # BASELINE.json configs[1] exactly: 512^3, const V, PML, Ricker, all 500
+    # steps, in the launch configuration bench.py times (stream kernels, CUDA
+    # graphs) -- the whole field against the oracle (~30 s on 16 host cores)
+    s = synth.scenario("C2")
+    g, gp = run_gpu(s, s.steps)
+    r, rp = run_oracle(s, s.steps)
+    e, ep = rel_linf(g, r), rel_linf(gp, rp)
+    print(f"C2 500 steps: rel Linf u^T {e:.3e}, u^(T-1) {ep:.3e}, max|u| {float(np.abs(r).max()):.4e}")
+    assert float(np.abs(r).max()) > 0 and e <= TOL and ep <= TOL, (e, ep)
+
+
 @pytest.mark.parametrize("seed", [0, 1, 2])
 @pytest.mark.parametrize("steps", [1, 10, 100])
 def test_c1_random_state(seed, steps):
