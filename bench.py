@@ -48,8 +48,13 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def workload(config: str, world: int):
+def workload(config: str, world: int, scaling: str = "weak"):
     import synth
+    if world > 1 and scaling == "strong":
+        s = synth.scenario("C3")
+        desc = (f"C4 strong scaling: the C3 1024^3 grid (layered V, 16-cell PML, Ricker 15 Hz at the "
+                f"centre) cut into {world} z-slabs of ~{1024 // world} planes (BASELINE.json configs[3])")
+        return s, desc
     if world > 1:
         s = synth.scenario("C5")
         s = s.with_(nz=s.nz * world)
@@ -185,7 +190,7 @@ def run_reference(args, rank, world):
         return
     import oracle
     oracle.build()
-    s, desc = workload(args.config, world)
+    s, desc = workload(args.config, world, args.scaling)
     total = args.steps + args.warmup
     planes = int(min(64, max(4, round(48 * 200 / max(total, 1)))))
     state = list(oracle_slab_setup(s, planes))
@@ -196,7 +201,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": desc, "sample_planes": planes},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
                          "sample": f"z-slab of {planes} planes x {args.steps} steps (+{args.warmup} warm-up)"},
@@ -266,7 +271,7 @@ def run_ours(args, rank, world, local):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    s, desc = workload(args.config, world)
+    s, desc = workload(args.config, world, args.scaling)
     off, nzl = slab_bounds(s.nz, rank, world) if world > 1 else (0, s.nz)
     V = synth.velocity(s, nz_global=s.nz, z_offset=off, nz_local=nzl)
     total_steps = args.warmup + 3 * args.steps + 8
@@ -398,7 +403,7 @@ def run_ours(args, rank, world, local):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64" if args.precision == "fp64" else "f32",
             "data": "synthetic",
             "config": {"workload": desc, "grid": [s.nx, s.ny, s.nz], "points_per_step": pts_total,
                        "pml_width": s.w, "parallelism": f"z-slab x{world}" if world > 1 else "1 GPU",
@@ -438,9 +443,11 @@ def main():
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N>1: weak = C5 (1024 planes per GPU), strong = C4 (the 1024^3 grid split N ways)")
     ap.add_argument("--repeats", type=int, default=5, help="timed runs (the first is `value`)")
     ap.add_argument("--kernel", choices=["stream", "tb2", "pair"], default="stream",
-                    help="1 GPU: stream (default) or tb2 two-step temporal blocking")
+                    help="1 GPU: stream (default), tb2 (two-step temporal blocking) or pair (two steps through L2)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = env_rank()
