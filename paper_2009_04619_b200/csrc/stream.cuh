@@ -50,7 +50,12 @@ struct Region {
 
 constexpr int MAX_REGIONS = 4;
 constexpr int SU = 9;           // u ring stages  (= 2R+1)
-constexpr int SP = 3;           // u_prev/vdt2 ring stages (divides 9)
+constexpr int SP = 3;           // u_prev/vdt2 ring stages of the TB2 kernel (divides 9)
+#ifndef W25_SP_MAX
+#define W25_SP_MAX 4            // deepest u_prev/vdt2 ring k_stream may use (A/B builds: -DW25_SP_MAX=3)
+#endif
+constexpr int W25_MAX_W = 512;  // largest PML width (the shared eta table holds 3 (w + 2) entries)
+constexpr int W25_SMEM_BUDGET = 232448 - 4096;   // 227 KB opt-in limit minus static shared memory
 
 struct StreamParams {
   void* out;                    // u_next buffer (= u_prev buffer), padded layout base (T)
@@ -146,8 +151,15 @@ struct StreamCfg {
   static constexpr int U_HALF = SW * SH;
   static constexpr int U_STAGE = NH * U_HALF;               // elements per u stage
   static constexpr int P_STAGE = CW * TY;                   // elements per u_prev / vdt2 stage
-  static constexpr int BAR_OFF = (SU * U_STAGE + 2 * SP * P_STAGE) * (int)sizeof(T);  // bytes
-  static constexpr int TAB_OFF = BAR_OFF + 2 * (SU + SP) * 8;
+  // u_prev / vdt2 ring depth: as deep as shared memory allows (3..W25_SP_MAX
+  // stages), so more of those two streams is in flight per SM
+  static constexpr int fits_(int n) {
+    return (SU * U_STAGE + 2 * n * P_STAGE) * (int)sizeof(T) + 2 * (SU + n) * 8 +
+               3 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
+  }
+  static constexpr int SPN = (W25_SP_MAX >= 5 && fits_(5)) ? 5 : (W25_SP_MAX >= 4 && fits_(4)) ? 4 : 3;
+  static constexpr int BAR_OFF = (SU * U_STAGE + 2 * SPN * P_STAGE) * (int)sizeof(T);  // bytes
+  static constexpr int TAB_OFF = BAR_OFF + 2 * (SU + SPN) * 8;
   static size_t smem_bytes(int w) { return TAB_OFF + 3 * (w + 2) * sizeof(T); }
   static_assert(CW % 4 == 0 && CW <= TX && TX % 4 == 0, "tile widths");
   static_assert(32 % LXW == 0 && (TY / TYT) % LYW == 0 && TY % TYT == 0, "warp tiling");
@@ -277,11 +289,11 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* su = reinterpret_cast<T*>(smem_raw);
   T* sup = su + SU * C::U_STAGE;
-  T* sv = sup + SP * C::P_STAGE;
+  T* sv = sup + C::SPN * C::P_STAGE;
   uint64_t* full_u = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF);
   uint64_t* empty_u = full_u + SU;
   uint64_t* full_p = empty_u + SU;
-  uint64_t* empty_p = full_p + SP;
+  uint64_t* empty_p = full_p + C::SPN;
   T* stab = reinterpret_cast<T*>(smem_raw + C::TAB_OFF);
   const int TABN = P.w + 2;
   // PAIR step 1: per-publication arrival counts of the consumer warps, in a ring
@@ -340,7 +352,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
 #pragma unroll
     for (int s = 0; s < SU; ++s) { mbar_init(&full_u[s], 1); mbar_init(&empty_u[s], C::NWC); }
 #pragma unroll
-    for (int s = 0; s < SP; ++s) { mbar_init(&full_p[s], 1); mbar_init(&empty_p[s], C::NWC); }
+    for (int s = 0; s < C::SPN; ++s) { mbar_init(&full_p[s], 1); mbar_init(&empty_p[s], C::NWC); }
     fence_mbar_init();
   }
   for (int i = tid; i < 3 * TABN; i += C::NT) stab[i] = static_cast<const T*>(P.tab)[i];
@@ -412,11 +424,11 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
     };
     for (int s = 0; s < SU; ++s)
       if (zs - R + s <= ze + R - 1) issue_u(zs - R + s, s);      // planes zs-4 .. zs+4
-    for (int s = 0; s < SP; ++s)
+    for (int s = 0; s < C::SPN; ++s)
       if (zs + s < ze) issue_p(zs + s, s);                       // planes zs .. zs+2
     // refill in release order: when plane t is released, u plane t+9 and p plane t+3 go in
 #pragma unroll 1
-    for (int t = zs - R; t + SU <= ze + R - 1 || t + SP < ze; ++t) {
+    for (int t = zs - R; t + SU <= ze + R - 1 || t + C::SPN < ze; ++t) {
       if (t + SU <= ze + R - 1) {
         const int o = t - zs + R;
         mbar_wait(&empty_u[o % SU], (o / SU) & 1);
@@ -425,14 +437,14 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
         fence_proxy_async_smem();
         issue_u(t + SU, o % SU);
       }
-      if (t >= zs && t + SP < ze) {
+      if (t >= zs && t + C::SPN < ze) {
         const int o = t - zs;
-        mbar_wait(&empty_p[o % SP], (o / SP) & 1);
+        mbar_wait(&empty_p[o % C::SPN], (o / C::SPN) & 1);
         fence_proxy_async_smem();
-        issue_p(t + SP, o % SP);
+        issue_p(t + C::SPN, o % C::SPN);
       }
       if (P.pf > 0) {
-        const int pu = t + SU + P.pf, pp = t + SP + P.pf;
+        const int pu = t + SU + P.pf, pp = t + C::SPN + P.pf;
         if (pu <= ze + R - 1)
 #pragma unroll
           for (int h = 0; h < C::NH; ++h) tma_prefetch_3d(mu, bx0 + h * C::HW - R, ty0 - R, pu + R);
@@ -659,8 +671,9 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
       }
 
       // 3. u^{n-1}, vdt2 of plane z
-      const int sp = s % 3;
-      mbar_wait(&full_p[sp], (j + s / 3) & 1);
+      const int po_ = 9 * j + s;             // plane index in the chunk
+      const int sp = po_ % C::SPN;
+      mbar_wait(&full_p[sp], (po_ / C::SPN) & 1);
       V upv[TYT], vv[TYT];
 #pragma unroll
       for (int r = 0; r < TYT; ++r) {

@@ -187,7 +187,7 @@ static void init_kernels() {
 #define KTY(ki) (g_k[P->prec][ki].ty)
 
 static constexpr double W8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0};
-static constexpr int MAX_W = 512;
+static constexpr int MAX_W = W25_MAX_W;
 
 struct Maps {
   CUtensorMap u[4];      // wavefield buffer b with halo box
