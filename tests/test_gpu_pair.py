@@ -139,3 +139,52 @@ def test_pair_z_chunks_and_publication_bitwise(monkeypatch, cz, pk, name, kw):
     (a, ap), _ = run(s, 10, "stream", u0, um1)
     (b, bp), spl = run(s, 10, "pair", u0, um1)
     assert spl == 2 and np.array_equal(a, b) and np.array_equal(ap, bp)
+
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("RAGGED", {}), ("RAGGED", dict(src=(6, 7, 9)))])
+def test_pair_fp64_equals_stream_fp64(name, kw):
+    # the fp64 instantiation of the pair kernel (124-wide tiles, double2 lanes)
+    from paper_2009_04619_b200.wave import WavePlan
+    s = synth.scenario(name, **kw)
+    sh = (s.nz, s.ny, s.nx)
+    u0 = synth.random_state(sh, 45).astype(np.float64)
+    outs = []
+    for kernel in ("stream", "pair"):
+        p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel, precision="fp64")
+        p.set_velocity(synth.velocity(s))
+        p.set_source(*s.source, synth.wavelet_for(s, 11))
+        p.set_state(None, u0)
+        p.step(11)
+        outs.append((p.read(0).cpu().numpy(), p.read(1).cpu().numpy(), p.steps_per_launch))
+        p.close()
+    (a, ap, sa), (b, bp, sb) = outs
+    assert sa == 1 and sb == 2 and a.dtype == np.float64
+    assert np.array_equal(a, b) and np.array_equal(ap, bp)
+
+
+def test_pair_with_stored_eta_falls_back_bitwise():
+    # a stored eta field disables the pair path (single steps, same values)
+    from paper_2009_04619_b200.wave import WavePlan
+    s = synth.scenario("RAGGED")
+    sh = (s.nz, s.ny, s.nx)
+    eta = np.full(sh, 1.5, np.float32)
+    u0 = synth.random_state(sh, 46)
+    outs = []
+    for kernel in ("stream", "pair"):
+        p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, kernel=kernel)
+        p.set_eta(eta)
+        p.set_velocity(synth.velocity(s))
+        p.set_source(*s.source, synth.wavelet_for(s, 9))
+        p.set_state(None, u0)
+        p.step(9)
+        outs.append((p.read(0).cpu().numpy(), p.steps_per_launch))
+        p.close()
+    assert outs[1][1] == 1 and np.array_equal(outs[0][0], outs[1][0])
+
+
+def test_pair_multislab_rejected():
+    from paper_2009_04619_b200._abi import WaveError
+    from paper_2009_04619_b200.wave import WavePlan
+    s = synth.scenario("RAGGED")
+    with pytest.raises(WaveError):
+        WavePlan(s.nx, s.ny, 30, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=0, kernel="pair")
