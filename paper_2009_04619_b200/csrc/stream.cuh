@@ -96,6 +96,7 @@ struct StreamParams {
                                 // 8 = per-block timeline records
   int pair_pk;                  // step 1 publishes its progress every pair_pk planes (and at the end)
   int64_t pair_dbg_off;         // timeline records (pair_dbg & 8) at prog + this, 6 u64 per block
+  int64_t pair_ticket;          // prog[pair_ticket]: next work unit (zeroed with the counters)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
@@ -301,7 +302,17 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   __shared__ unsigned s_arr[PAIR ? 16 : 1];
 
   // ---- work unit ---------------------------------------------------------
-  int b = blockIdx.x, ri = 0;
+  // PAIR: work units are handed out by a ticket counter in CTA start order, so
+  // a step-2 unit only ever waits on units already taken by running (or
+  // finished) CTAs -- deadlock-free whatever order the hardware dispatches in
+  int unit = blockIdx.x;
+  if (PAIR) {
+    __shared__ int s_unit;
+    if (threadIdx.x == 0) s_unit = (int)atomicAdd(P.prog + P.pair_ticket, 1u);
+    __syncthreads();
+    unit = s_unit;
+  }
+  int b = unit, ri = 0;
 #pragma unroll 1
   while (ri + 1 < P.nreg && b >= P.reg[ri + 1].blk0) ++ri;
   const Region& G = P.reg[ri];
@@ -313,11 +324,11 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   int role = 0;                          // PAIR: 1 = step 1, 2 = step 2
   if (PAIR) {
     // groups of one tile row each, in dependency order (S1 r+1 before S2 r)
-    const int g = blockIdx.x / G.ntx, code = P.pair_groups[g];
+    const int g = unit / G.ntx, code = P.pair_groups[g];
     role = code >> 28;
     zc = (code >> 16) & 0xfff;
     tyi = code & 0xffff;
-    txi = blockIdx.x - g * G.ntx;
+    txi = unit - g * G.ntx;
   } else if (P.order <= 0) {
     tyi = rem / G.ntx;
     txi = rem - tyi * G.ntx;
@@ -459,7 +470,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      unsigned long long* rec = reinterpret_cast<unsigned long long*>(P.prog + P.pair_dbg_off) + 6 * blockIdx.x;
+      unsigned long long* rec = reinterpret_cast<unsigned long long*>(P.prog + P.pair_dbg_off) + 6 * unit;
       rec[0] = ((unsigned long long)role << 48) | ((unsigned long long)zc << 32) | ((unsigned)tyi << 16) | txi;
       rec[1] = smid;
       rec[2] = dbg_t0;

@@ -569,9 +569,10 @@ static wave_status build_launches(wave_plan* P) {
       CK(cudaMalloc(&P->pair_groups_d, groups.size() * sizeof(int)));
       CK(cudaMemcpy(P->pair_groups_d, groups.data(), groups.size() * sizeof(int), cudaMemcpyHostToDevice));
       const int64_t ndbg = (P->pair_dbg & 8) ? 12 * (int64_t)L.nblk + 2 : 0;   // u32 words, u64-aligned
-      L.p.pair_dbg_off = (ntile + 1) & ~(int64_t)1;
+      L.p.pair_ticket = ntile;                              // after the per-tile counters
+      L.p.pair_dbg_off = (ntile + 2) & ~(int64_t)1;
       CK(cudaMalloc(&P->prog_d, (L.p.pair_dbg_off + ndbg) * sizeof(unsigned)));
-      P->prog_n = ntile;
+      P->prog_n = ntile + 1;                                // counters + ticket, zeroed per launch
       L.p.pair_groups = P->pair_groups_d;
       L.p.prog = P->prog_d;
       P->pair_launch = L;
