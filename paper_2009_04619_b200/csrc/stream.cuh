@@ -65,7 +65,8 @@ struct StreamParams {
   int nx, ny, nzl, nzg, zoff, w;
   int cz;                       // z-chunk length
   int pf;                       // L2 prefetch distance (planes beyond the rings; 0 = off)
-  int order;                    // tile order in a chunk: 0 = x fastest; G > 0 = groups of G x-tiles, y inside
+  int order;                    // tile order in a chunk: 0 = x fastest; G > 0 = groups of G x-tiles, y inside;
+                                // -B = bands of B tile rows, y fastest inside a band
   int upol;                     // L2 policy of u loads: 0 = evict_last, 1 = evict_normal
   int nreg;
   Region reg[MAX_REGIONS];
@@ -329,7 +330,14 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
     zc = (code >> 16) & 0xfff;
     tyi = code & 0xffff;
     txi = unit - g * G.ntx;
-  } else if (P.order <= 0) {
+  } else if (P.order < 0) {                // bands of -order tile rows, x-major inside a band
+    const int bh = -P.order;
+    const int band = rem / (bh * G.ntx);
+    const int bsz = min(bh, G.nty - band * bh);
+    const int r2 = rem - band * bh * G.ntx;
+    txi = r2 / bsz;
+    tyi = band * bh + (r2 - txi * bsz);
+  } else if (P.order == 0) {
     tyi = rem / G.ntx;
     txi = rem - tyi * G.ntx;
   } else {                                 // groups of P.order x-tiles; inside a group y-major
