@@ -303,7 +303,13 @@ def run_ours(args, rank, world, local):
     if world == 1:
         runner = None
     elif halo == "peer":
-        runner = PeerSlabRunner(plan, rank, world)
+        try:
+            runner = PeerSlabRunner(plan, rank, world)
+        except RuntimeError as e:       # no P2P path: the NCCL send/recv path instead (all ranks agree)
+            print(f"[bench] fused peer exchange unavailable ({e}); using NCCL send/recv", file=sys.stderr)
+            halo = "nccl"
+            runner = SlabRunner(plan, rank, world,
+                                stage_on_host=os.environ.get("WAVE25_DIST_BACKEND", "nccl") != "nccl")
     else:
         runner = SlabRunner(plan, rank, world,
                             stage_on_host=os.environ.get("WAVE25_DIST_BACKEND", "nccl") != "nccl")

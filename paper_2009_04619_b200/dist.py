@@ -181,24 +181,44 @@ class PeerSlabRunner:
         lo = allv[rank - 1] if rank > 0 else None
         hi = allv[rank + 1] if rank < world - 1 else None
         dev = plan.device
-        self._lo = (_PeerBuf(lo[0], dev), _PeerBuf(lo[1], dev), _PeerBuf(lo[2], dev), lo[3]) if lo else None
-        self._hi = (_PeerBuf(hi[0], dev), _PeerBuf(hi[1], dev), _PeerBuf(hi[2], dev), hi[3]) if hi else None
-        plan.set_peers(lo_bufs=self._lo[:2] if self._lo else None, hi_bufs=self._hi[:2] if self._hi else None,
-                       lo_nz=self._lo[3] if self._lo else 0, lo_flags=self._lo[2] if self._lo else None,
-                       hi_flags=self._hi[2] if self._hi else None)
+        self._lo = self._hi = None
+        err = None
+        try:
+            self._lo = (_PeerBuf(lo[0], dev), _PeerBuf(lo[1], dev), _PeerBuf(lo[2], dev), lo[3]) if lo else None
+            self._hi = (_PeerBuf(hi[0], dev), _PeerBuf(hi[1], dev), _PeerBuf(hi[2], dev), hi[3]) if hi else None
+            plan.set_peers(lo_bufs=self._lo[:2] if self._lo else None,
+                           hi_bufs=self._hi[:2] if self._hi else None,
+                           lo_nz=self._lo[3] if self._lo else 0, lo_flags=self._lo[2] if self._lo else None,
+                           hi_flags=self._hi[2] if self._hi else None)
+        except Exception as e:          # e.g. no P2P path between two GPUs
+            err = e
+        # every rank learns whether every rank is wired (a collective all reach,
+        # so a failure on one rank cannot leave the others waiting)
+        flag = torch.tensor([0 if err else 1], dtype=torch.int32,
+                            device=plan.device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) == 0:
+            self._unwire()
+            raise RuntimeError(f"peer wiring failed on at least one rank (this rank: {err!r})")
         self._barrier()
+
+    def _unwire(self) -> None:
+        try:
+            self.plan.clear_peers()
+        finally:
+            for side in (self._lo, self._hi):
+                if side:
+                    for b in side[:3]:
+                        if isinstance(b, _PeerBuf):
+                            b.release()
+            self._lo = self._hi = None
 
     def close(self) -> None:
         """Unwire the plan and unmap the neighbours' buffers (collective: every
         rank calls it after its last step; the barrier keeps each mapping alive
         until no rank can still be storing through it)."""
         self._barrier()
-        self.plan.clear_peers()
-        for side in (self._lo, self._hi):
-            if side:
-                for b in side[:3]:
-                    b.release()
-        self._lo = self._hi = None
+        self._unwire()
 
     def _barrier(self):
         torch.cuda.synchronize(self.plan.device)

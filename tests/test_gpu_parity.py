@@ -487,6 +487,65 @@ def _peer_worker(rank, world, port, steps, q):
         dist.destroy_process_group()
 
 
+def _peer_fail_worker(rank, world, port, q):
+    # rank 1 cannot wire its peers: both ranks must get the error (no hang),
+    # unwire, and the NCCL-path SlabRunner (gloo here) still gives the right field
+    import os
+    import torch.distributed as dist
+    from paper_2009_04619_b200.dist import PeerSlabRunner, SlabRunner, slab_bounds
+    from paper_2009_04619_b200.wave import WavePlan as WP
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        s = synth.scenario("RAGGED")
+        off, nzl = slab_bounds(s.nz, rank, world)
+        p = WP(s.nx, s.ny, nzl, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=off)
+        p.set_velocity(synth.velocity(s)[off:off + nzl])
+        p.set_source(*s.source, synth.wavelet_for(s, 7))
+        if rank == 1:
+            def boom(*a, **k):
+                raise RuntimeError("simulated: no P2P path")
+            p.set_peers = boom
+        raised = False
+        try:
+            PeerSlabRunner(p, rank, world)
+        except RuntimeError:
+            raised = True
+        runner = SlabRunner(p, rank, world, stage_on_host=True)
+        runner.step(7)
+        torch.cuda.synchronize()
+        q.put((rank, raised, p.read(0).cpu().numpy()))
+        dist.barrier()
+        p.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_wiring_failure_is_collective():
+    import socket
+    import torch.multiprocessing as mp
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    parts = sorted((q.get(timeout=300) for _ in range(2)), key=lambda t: t[0])
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    assert all(raised for _, raised, _ in parts)
+    got = np.concatenate([a for _, _, a in parts], axis=0)
+    s = synth.scenario("RAGGED")
+    ref, _ = run_gpu(s, 7, wl=synth.wavelet_for(s, 7))
+    assert np.array_equal(got, ref)
+
+
 def test_peer_slab_runner_two_processes_bitwise():
     # the production multi-GPU path (IPC-mapped neighbour buffers, peer stores,
     # device flags) with 2 processes sharing one GPU == the single-plan run
