@@ -73,14 +73,17 @@ typedef enum { WAVE_MEM_HOST = 0, WAVE_MEM_DEVICE = 1 } wave_mem;
  * steps reading u^n, u^{n-1}, vdt2 once (10 B per point-step instead of 16);
  * it needs two extra wavefield buffers (wave_plan_bind_aux) and a single-slab
  * plan, and falls back to STREAM single steps otherwise (odd step counts end
- * with one STREAM step).  All three compute bitwise-identical values. */
+ * with one STREAM step).  All four compute bitwise-identical values. */
 typedef enum { WAVE_KERNEL_STREAM = 0, WAVE_KERNEL_NAIVE = 1, WAVE_KERNEL_TB2 = 2, WAVE_KERNEL_PAIR = 3 } wave_kernel;
 /* WAVE_KERNEL_PAIR: two steps per interior launch with no
- * redundant work: step-1 blocks publish per-plane progress, step-2 blocks of
- * the same launch wait for their own and neighbouring tiles and read u^{n+1}
- * back through L2; walls run as single steps before and after.  In place
- * (two buffers), single-slab plans, falls back to STREAM with a stored eta.
- * Bitwise equal to STREAM. */
+ * redundant work: step-1 blocks publish per-tile, per-z-chunk progress,
+ * step-2 blocks of the same launch wait for their own and neighbouring tiles
+ * and read u^{n+1} back through L2; CTAs take work units from a ticket
+ * counter in start order (deadlock-free); walls run as single steps before
+ * and after.  In place (two buffers), single-slab plans only (CONFIG error
+ * otherwise), fp32 and fp64, falls back to STREAM single steps with a stored
+ * eta.  Bitwise equal to STREAM.  Measured slower than STREAM on B200 (kept
+ * as an ablation). */
 
 /* Arithmetic / storage precision of a plan.  FP32 (default): every constant
  * computed in fp64 and rounded once to fp32 (R8), fp32 storage and
