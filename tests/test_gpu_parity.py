@@ -659,3 +659,32 @@ def test_ipc_export_offsets():
     h0, o0 = _abi.wave_ipc_export(t.data_ptr())
     h1, o1 = _abi.wave_ipc_export(t[1000:].data_ptr())
     assert len(h0) == 64 and h0 == h1 and o1 - o0 == 4000
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_mirror_symmetry_bitwise_full_size(precision):
+    # odd extents (511^3), centred source, constant V, a mirror-symmetric O(1)
+    # initial state that loads every PML wall from step 1: the field stays
+    # bitwise mirror-symmetric along every axis (pair sums before multiplying,
+    # the eta star's two differences flip sign together).  Catches an
+    # off-by-one in a wall region, a one-sided tile edge or halo, or an
+    # asymmetric z cap, on the full-size launch configuration.
+    n, h = 511, 256
+    s = synth.scenario("C2", nx=n, ny=n, nz=n, src=(n // 2, n // 2, n // 2))
+    rng = np.random.Generator(np.random.PCG64(91))
+    q = rng.uniform(-1, 1, size=(h, h, h))
+    for ax in range(3):
+        q = np.concatenate([q, np.flip(q, axis=ax).take(range(1, h), axis=ax)], axis=ax)
+    dtype = np.float64 if precision == "fp64" else np.float32
+    u0 = q.astype(dtype)
+    assert all(np.array_equal(u0, np.flip(u0, axis=ax)) for ax in range(3))
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, precision=precision)
+    p.set_velocity(np.full((n, n, n), 2000.0, np.float32))
+    p.set_source(*s.source, synth.wavelet_for(s, 30))
+    p.set_state(u0, u0)
+    p.step(30)
+    u = p.read(0).cpu().numpy()
+    p.close()
+    assert np.isfinite(u).all() and np.abs(u).max() > 0
+    for ax in range(3):
+        assert np.array_equal(u, np.flip(u, axis=ax)), ax
