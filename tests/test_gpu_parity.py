@@ -258,12 +258,12 @@ def test_auto_dt_matches_oracle_rule():
     p.close()
 
 
-def _full_size_slab_check(sname, steps, zt_list, seed=0, kernel="stream"):
+def _full_size_slab_check(sname, steps, zt_list, seed=0, kernel="stream", **kw):
     """Full-size GPU run; oracle recomputes sampled z-slabs.  The oracle slab
     is the target planes plus 4*steps planes of margin on each side, whose
     ghost planes hold the initial state: after `steps` steps the target planes
     are exact (the contamination from stale ghosts moves 4 planes per step)."""
-    s = synth.scenario(sname)
+    s = synth.scenario(sname, **kw)
     sh = (s.nz, s.ny, s.nx)
     u0 = synth.random_state(sh, seed)
     um1 = synth.random_state(sh, seed + 1)
@@ -299,6 +299,15 @@ def _full_size_slab_check(sname, steps, zt_list, seed=0, kernel="stream"):
         worst = max(worst, rel_linf(got, ref))
     p.close()
     return worst
+
+
+@pytest.mark.parametrize("kernel", ["stream", "pair"])
+def test_beyond_2g_elements_sampled_slabs(kernel):
+    # 2048 x 2048 x 520 (2.18e9 points per buffer > 2^31): every index and
+    # offset on the path must be 64-bit; sampled slabs incl. both z caps
+    err = _full_size_slab_check("C2", 4, [(0, 12), (254, 266), (508, 520)], seed=5, kernel=kernel,
+                                nx=2048, ny=2048, nz=520)
+    assert err <= TOL, err
 
 
 @pytest.mark.parametrize("sname,kernel", [("C2", "stream"), ("C3", "stream"), ("C2", "tb2"), ("C3", "tb2"),
