@@ -301,7 +301,7 @@ def _full_size_slab_check(sname, steps, zt_list, seed=0, kernel="stream", **kw):
     return worst
 
 
-@pytest.mark.parametrize("kernel", ["stream", "pair"])
+@pytest.mark.parametrize("kernel", ["stream", "pair", "tb2"])
 def test_beyond_2g_elements_sampled_slabs(kernel):
     # 2048 x 2048 x 520 (2.18e9 points per buffer > 2^31): every index and
     # offset on the path must be 64-bit; sampled slabs incl. both z caps
