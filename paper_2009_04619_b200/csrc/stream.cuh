@@ -277,12 +277,14 @@ __device__ __noinline__ typename VecT<T>::V pml_row_eta(typename VecT<T>::V L, t
   return vmake<T>(res);
 }
 
+// The body of one work unit (tile x z-chunk) of k_stream; `unit0` = its index
+// in the launch's region list (blockIdx.x for k_stream, remapped by k_mix).
 template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0, typename T = float, int PAIR = 0>
-__global__ void __maxnreg__((StreamCfg<TX, CW, TY, TYT, MINB, RA, T>::MAXR))
-k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1)
-         const __grid_constant__ CUtensorMap tm_up,   // u^{n-1}, box (CW, TY, 1)
-         const __grid_constant__ CUtensorMap tm_v,    // vdt2, box (CW, TY, 1)
-         const __grid_constant__ StreamParams P) {
+__device__ __forceinline__ void
+stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
+            const CUtensorMap& tm_up,   // u^{n-1}, box (CW, TY, 1)
+            const CUtensorMap& tm_v,    // vdt2, box (CW, TY, 1)
+            const StreamParams& P, const int unit0) {
   using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T>;
   using V = typename VecT<T>::V;
   constexpr int NV = C::NV;
@@ -306,7 +308,7 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
   // PAIR: work units are handed out by a ticket counter in CTA start order, so
   // a step-2 unit only ever waits on units already taken by running (or
   // finished) CTAs -- deadlock-free whatever order the hardware dispatches in
-  int unit = blockIdx.x;
+  int unit = unit0;
   if (PAIR) {
     __shared__ int s_unit;
     if (threadIdx.x == 0) s_unit = (int)atomicAdd(P.prog + P.pair_ticket, 1u);
@@ -862,6 +864,53 @@ k_stream(const __grid_constant__ CUtensorMap tm_u,    // u^n, box (HW+8, TY+8, 1
       }
       optr += P.plane;
     }
+  }
+}
+
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0, typename T = float, int PAIR = 0>
+__global__ void __maxnreg__((StreamCfg<TX, CW, TY, TYT, MINB, RA, T>::MAXR))
+k_stream(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
+         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ StreamParams P) {
+  stream_body<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR>(tm_u, tm_up, tm_v, P, blockIdx.x);
+}
+
+// ---------------------------------------------------------------------------
+// k_mix: the interior launch and the x-wall launch as ONE grid.
+// Work units of both are interleaved chunk by chunk: z-chunk c holds the
+// interior's tiles (tile-row order) with the x-wall tiles of the same rows
+// slotted in next to them, so a wall CTA streams its 64-B row pieces while the
+// interior CTAs of the same rows and planes open the same DRAM pages and read
+// the same halo columns through L2.  Every CTA is uniformly interior or wall
+// (no per-warp paths); both bodies are the unchanged k_stream bodies, which
+// need the same block size and register cap (checked on the host).
+struct MixParams {
+  StreamParams pi, pw;          // interior / x-wall launch parameters (same cz, same z range)
+  const int* seq;               // per chunk position: >= 0 interior tile, < 0 -(1 + wall tile)
+  int per_chunk;                // interior tiles + wall tiles per z-chunk
+  int ni;                       // interior tiles per z-chunk
+};
+
+template <int TXI, int TYI, int TXW, int CWW, int TYW, int RA>
+__global__ void __maxnreg__((StreamCfg<TXI, TXI, TYI, 1, 1, RA, float>::MAXR))
+k_mix(const __grid_constant__ CUtensorMap ti_u, const __grid_constant__ CUtensorMap ti_up,
+      const __grid_constant__ CUtensorMap ti_v, const __grid_constant__ CUtensorMap tw_u,
+      const __grid_constant__ CUtensorMap tw_up, const __grid_constant__ CUtensorMap tw_v,
+      const __grid_constant__ MixParams M) {
+  static_assert(StreamCfg<TXI, TXI, TYI, 1, 1, RA, float>::NT == StreamCfg<TXW, CWW, TYW, 1, 1, RA, float>::NT,
+                "interior and wall bodies need the same block size");
+  const int c = blockIdx.x / M.per_chunk;
+  const int q = M.seq[blockIdx.x - c * M.per_chunk];
+  if (q >= 0) {
+    stream_body<TXI, TXI, TYI, 1, MODE_INNER, 1, RA, float, 0>(ti_u, ti_up, ti_v, M.pi, c * M.ni + q);
+  } else {
+    // wall tile s of chunk c: region s / ncol, tile s % ncol (regions are
+    // region-major in the wall launch's own numbering)
+    const int s = -q - 1;
+    const Region& g0 = M.pw.reg[0];
+    const int ncol = g0.ntx * g0.nty;
+    const int r = s / ncol;
+    stream_body<TXW, CWW, TYW, 1, MODE_WALL, 1, RA, float, 0>(tw_u, tw_up, tw_v, M.pw,
+                                                             M.pw.reg[r].blk0 + c * ncol + (s - r * ncol));
   }
 }
 

@@ -149,6 +149,10 @@ enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_WALLX_E = 4, K
 static bool is_wall(int ki) { return ki == KI_WALLX || ki == KI_WALLY || ki == KI_WALLX_E || ki == KI_WALLY_E; }
 
 static KInfo g_k[2][KI_N];   // [precision: 0 fp32, 1 fp64][kernel kind]
+// the two bodies k_mix instantiates: the default interior and x-wall kernels
+static KInfo mix_inner() { return kinfo<248, 248, 8, 1, MODE_INNER, 1, 112>("248x8x1r"); }
+static KInfo mix_wallx() { return kinfo<24, 16, 128, 1, MODE_WALL, 1, 112>("x24c16x128x1r"); }
+static void* mix_fn() { return (void*)k_mix<248, 8, 24, 16, 128, 112>; }
 static void init_kernels() {
   static bool done = false;
   if (done) return;
@@ -283,6 +287,11 @@ struct wave_plan {
   int wall_cz = 0;                   // WAVE25_WALL_CZ: wall chunk length (0 = auto)
   int xwall_extra = 0;               // WAVE25_XWALL_EXTRA: inner columns computed by the x-wall kernel
   bool walls_last = false;           // WAVE25_WALLS_LAST: enqueue the wall kernels after the interior
+  int mix = 0;                       // WAVE25_MIX=1/2: interior + x walls as one grid (k_mix, §5i; measured slower)
+  bool mix_ok = false;               // geometry / kernel choice supports k_mix (set by build_launches)
+  int* mix_seq_d = nullptr;          // k_mix chunk sequence (device)
+  MixParams mixp{};
+  int mix_nblk = 0;
   cudaGraphExec_t gexec[16] = {};    // 2-step graphs keyed by (cur, prv)
   // two-step temporal blocking (WAVE_KERNEL_TB2)
   T2Info t2{};
@@ -534,6 +543,64 @@ static wave_status build_launches(wave_plan* P) {
       add_regions(P, ky, {{xw, nx - xw, 0, w}, {xw, nx - xw, ny - w, ny}}, *sets[s], &P->launches[s]);
     }
   }
+  // interior + x walls as one grid (k_mix): the x-wall launch
+  // takes the interior's z-chunks; chunk by chunk, the wall tiles go next to
+  // the interior tile rows they border
+  P->mix_ok = false;
+  if (P->mix && P->prec == 0 && !P->eta_on && !P->fused && !P->xfuse && P->xwall_extra == 0 && w > 0 &&
+      g_k[0][KI_INNER].fn == mix_inner().fn && g_k[0][KI_WALLX].fn == mix_wallx().fn) {
+    Launch* Li = nullptr;
+    Launch* Lx = nullptr;
+    for (Launch& L : P->launches[0]) {
+      if (L.ki == KI_INNER) Li = Li ? nullptr : &L;
+      if (L.ki == KI_WALLX) Lx = Lx ? nullptr : &L;
+    }
+    if (Li && Lx && Li->p.nreg == 1 && Lx->p.nreg == 2) {
+      const Region& gi = Li->p.reg[0];
+      StreamParams& pw = Lx->p;
+      const int cz = Li->p.cz, ncw = pw.reg[0].ntx * pw.reg[0].nty;
+      bool ok = pw.reg[1].ntx * pw.reg[1].nty == ncw && pw.reg[0].ntx == 1;
+      int blk = 0;
+      for (int r = 0; r < 2 && ok; ++r) {
+        Region& g = pw.reg[r];
+        ok = g.z0 == gi.z0 && g.z1 == gi.z1;
+        g.nzc = (g.z1 - g.z0 + cz - 1) / cz;
+        g.blk0 = blk;
+        blk += ncw * g.nzc;
+      }
+      if (ok && pw.reg[0].nzc == gi.nzc) {
+        pw.cz = cz;
+        Lx->nblk = blk;
+        // chunk sequence: interior tiles in tile-row order; wall tile t of
+        // each side right after the interior row holding its middle y
+        const int ni = gi.ntx * gi.nty;
+        std::vector<std::vector<int>> after(gi.nty);
+        for (int r = 0; r < 2; ++r)
+          for (int t = 0; t < ncw; ++t) {
+            const int ymid = pw.reg[r].y0 + t * g_k[0][KI_WALLX].ty + g_k[0][KI_WALLX].ty / 2;
+            const int row = std::max(0, std::min(gi.nty - 1, (ymid - gi.y0) / g_k[0][KI_INNER].ty));
+            after[row].push_back(-(1 + r * ncw + t));
+          }
+        std::vector<int> seq;
+        if (P->mix == 2)                  // WAVE25_MIX=2: every wall tile at the start of its chunk
+          for (int row = 0; row < gi.nty; ++row) { seq.insert(seq.end(), after[row].begin(), after[row].end()); after[row].clear(); }
+        for (int row = 0; row < gi.nty; ++row) {
+          for (int tx = 0; tx < gi.ntx; ++tx) seq.push_back(row * gi.ntx + tx);
+          for (int q : after[row]) seq.push_back(q);
+        }
+        if (P->mix_seq_d) { cudaFree(P->mix_seq_d); P->mix_seq_d = nullptr; }
+        CK(cudaMalloc(&P->mix_seq_d, seq.size() * sizeof(int)));
+        CK(cudaMemcpy(P->mix_seq_d, seq.data(), seq.size() * sizeof(int), cudaMemcpyHostToDevice));
+        P->mixp.pi = Li->p;
+        P->mixp.pw = pw;
+        P->mixp.seq = P->mix_seq_d;
+        P->mixp.per_chunk = (int)seq.size();
+        P->mixp.ni = ni;
+        P->mix_nblk = (int)seq.size() * gi.nzc;
+        P->mix_ok = true;
+      }
+    }
+  }
   // two-step temporal blocking: interior launch over the (w+4)-shrunk inner xy
   // box, walls in two single-step phases over frames of width w+8 and w+4
   // two steps through L2: one launch over the inner xy footprint x all z,
@@ -771,6 +838,33 @@ static wave_status launch_stream(wave_plan* P, const Launch& Lc, int ui, int upi
   return WAVE_OK;
 }
 
+// interior + x walls in one grid
+static bool mix_active(const wave_plan* P) {
+  return P->mix_ok && !P->remote && !(P->gmaps && P->maps_g) && P->l2_persist_mb == 0 && !ablation_shape();
+}
+
+static wave_status launch_mix(wave_plan* P, int ui, int upi, float* out, cudaStream_t s) {
+  const Maps& Mi = P->maps[KI_INNER];
+  const Maps& Mw = P->maps[KI_WALLX];
+  MixParams m = P->mixp;
+  m.pi.out = m.pw.out = out;
+  m.pi.rlo = m.pi.rhi = m.pw.rlo = m.pw.rhi = nullptr;
+  void* args[] = {(void*)&Mi.u[ui], (void*)&Mi.up[upi], (void*)&Mi.v,
+                  (void*)&Mw.u[ui], (void*)&Mw.up[upi], (void*)&Mw.v, (void*)&m};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(P->mix_nblk);
+  cfg.blockDim = dim3(kernel_threads(P, KI_INNER));
+  cfg.dynamicSmemBytes = std::max(kernel_smem(P, KI_INNER), kernel_smem(P, KI_WALLX));
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = P->prio_lo;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelExC(&cfg, mix_fn(), args));
+  return WAVE_OK;
+}
+
 static wave_status launch_naive(wave_plan* P, int cur, int prv, int z0, int z1, cudaStream_t s) {
   if (z1 <= z0) return WAVE_OK;
   NaiveParams np;
@@ -833,18 +927,20 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cu
   }
   const std::vector<Launch>& Ls = P->launches[which];
   if (Ls.empty()) return WAVE_OK;
+  const bool mix = which == 0 && mix_active(P);
+  auto mixed_out = [&](int ki) { return mix && (ki == KI_INNER || ki == KI_WALLX); };
   // fork BEFORE any launch: the wall kernels (side stream, high priority) and
   // the interior kernel (stream s) run concurrently; join before the source
   bool walls = false;
   for (const Launch& L : Ls) walls |= is_wall(L.ki);
   if (walls && P->serial) {                 // WAVE25_SERIAL=1: everything on `s`, walls first
     for (const Launch& L : Ls)
-      if (is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+      if (is_wall(L.ki) && !mixed_out(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
     walls = false;
   }
   auto launch_walls = [&]() -> wave_status {
     for (const Launch& L : Ls)
-      if (is_wall(L.ki)) {
+      if (is_wall(L.ki) && !mixed_out(L.ki)) {
         const bool y = L.ki == KI_WALLY || L.ki == KI_WALLY_E;
         CKST(launch_stream(P, L, cur, prv, P->buf[prv], (y && P->side2_on) ? P->side2 : P->side));
       }
@@ -856,8 +952,9 @@ static wave_status enqueue_compute(wave_plan* P, int which, int cur, int prv, cu
     if (P->side2_on) CK(cudaStreamWaitEvent(P->side2, P->ev_fork, 0));
     if (!P->walls_last) CKST(launch_walls());
   }
+  if (mix) CKST(launch_mix(P, cur, prv, P->buf[prv], s));
   for (const Launch& L : Ls)
-    if (!is_wall(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
+    if (!is_wall(L.ki) && !mixed_out(L.ki)) CKST(launch_stream(P, L, cur, prv, P->buf[prv], s));
   if (walls && P->walls_last) CKST(launch_walls());
   if (P->serial) return WAVE_OK;
   if (walls) {
@@ -1208,6 +1305,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
   if (const char* e = getenv("WAVE25_WALLS_LAST")) P->walls_last = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_MIX")) P->mix = atoi(e);
   if (const char* e = getenv("WAVE25_GMAPS")) P->gmaps = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
   if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;
@@ -1245,6 +1343,12 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel_ptr(P, ki), kernel_threads(P, ki), sm);
     P->occ[ki] = std::max(1, occ);
   }
+  {
+    const size_t sm = std::max(kernel_smem(P, KI_INNER), kernel_smem(P, KI_WALLX));
+    if (P->prec == 0 &&
+        (e = cudaFuncSetAttribute(mix_fn(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess)
+      return bail(fail(WAVE_ERR_CUDA, "smem attribute (mix): %s", cudaGetErrorString(e)));
+  }
   if (P->d.kernel == WAVE_KERNEL_TB2) {
     P->t2 = pick_t2();
     const size_t sm = P->t2.smem(P->d.pml_width);
@@ -1279,6 +1383,7 @@ void wave_plan_destroy(wave_plan* P) {
     }
   }
   if (P->pair_groups_d) cudaFree(P->pair_groups_d);
+  if (P->mix_seq_d) cudaFree(P->mix_seq_d);
   if (P->prog_d) cudaFree(P->prog_d);
   if (P->dstep) cudaFree(P->dstep);
   if (P->stats_d) cudaFree(P->stats_d);
