@@ -266,6 +266,7 @@ struct wave_plan {
   int occ[KI_N] = {1, 1, 1, 1, 1, 1, 1};
   bool fused = false;                // WAVE25_FUSED=1: one launch, per-warp paths (measured slower)
   int pf = 1;                        // L2 prefetch distance (WAVE25_PF), measured best
+  int wall_pf = -1;                  // wall kernels' L2 prefetch distance (WAVE25_WALL_PF; -1 = pf)
   int prio_lo = 0, prio_hi = 0;      // stream priority range (launch attribute)
   bool wall_prio = true;             // WAVE25_WALL_PRIO=0 disables
   bool serial = false;               // WAVE25_SERIAL=1: walls and interior on one stream (diagnostic)
@@ -338,12 +339,24 @@ static wave_status get_encoder() {
   return WAVE_OK;
 }
 
-// L2 sector promotion of TMA loads (WAVE25_L2PROMO = 0 none, 1 64B, 2 128B, 3 256B)
-static CUtensorMapL2promotion l2_promotion() {
+// promotion of the centre-only (u_prev, vdt2) loads of kernel kind ki:
+// WAVE25_WALL_L2PROMO for wall kernels whose rows are narrower than 128 B
+static int centre_promo(const wave_plan* P, int ki, uint32_t cw) {
   static int v = [] {
+    const char* e = getenv("WAVE25_WALL_L2PROMO");
+    return e ? atoi(e) : -1;
+  }();
+  return (is_wall(ki) && cw * P->esz < 128) ? v : -1;
+}
+
+// L2 sector promotion of TMA loads (WAVE25_L2PROMO = 0 none, 1 64B, 2 128B, 3 256B);
+// `v` >= 0 overrides it for one map
+static CUtensorMapL2promotion l2_promotion(int v = -1) {
+  static int dflt = [] {
     const char* e = getenv("WAVE25_L2PROMO");
     return e ? atoi(e) : 2;
   }();
+  if (v < 0) v = dflt;
   switch (v) {
     case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
     case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
@@ -354,14 +367,14 @@ static CUtensorMapL2promotion l2_promotion() {
 
 static wave_status encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                             uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t b0, uint32_t b1,
-                            bool f64 = false) {
+                            bool f64 = false, int promo = -1) {
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = g_encode(m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
                         dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(),
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(promo),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(WAVE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return WAVE_OK;
@@ -713,7 +726,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   p.eta = P->eta_on ? P->eta_buf : nullptr;
   p.dt = (double)P->dt;
   p.cz = cz;
-  p.pf = P->pf;
+  p.pf = (is_wall(ki) && P->wall_pf >= 0) ? P->wall_pf : P->pf;
   p.order = P->order;
   p.upol = P->upol;
   int blk = 0;
@@ -1306,6 +1319,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
   if (const char* e = getenv("WAVE25_WALLS_LAST")) P->walls_last = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_MIX")) P->mix = atoi(e);
+  if (const char* e = getenv("WAVE25_WALL_PF")) P->wall_pf = atoi(e);
   if (const char* e = getenv("WAVE25_GMAPS")) P->gmaps = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
   if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;
@@ -1420,7 +1434,8 @@ static wave_status encode_buffer(wave_plan* P, int b) {
     const uint32_t TX = KTX(ki), CW = KCW(ki), TY = KTY(ki);
     CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R,
                   f64));
-    CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY, f64));
+    CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY, f64,
+                  centre_promo(P, ki, CW)));
   }
   if (P->d.kernel == WAVE_KERNEL_TB2) {
     const uint32_t TX = P->t2.tx, TY = P->t2.ty;
@@ -1453,7 +1468,8 @@ wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
   const uint64_t pb = P->L.pitch_x * P->esz, plb = pb * P->d.ny;
   for (int ki = 0; ki < KI_N; ++ki)
-    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, KCW(ki), KTY(ki), P->prec == 1));
+    CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, KCW(ki), KTY(ki), P->prec == 1,
+                  centre_promo(P, ki, KCW(ki))));
   if (P->d.kernel == WAVE_KERNEL_TB2) {
     CKST(encode3d(&P->t2maps.v1, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, P->t2.tx + 2 * R, P->t2.ty + 2 * R));
     CKST(encode3d(&P->t2maps.v2, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, P->t2.tx, P->t2.ty));
