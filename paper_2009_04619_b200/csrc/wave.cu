@@ -489,12 +489,13 @@ static int kernel_threads(const wave_plan* P, int ki) { return g_k[P->prec][ki].
 static size_t kernel_smem(const wave_plan* P, int ki) { return g_k[P->prec][ki].smem(P->d.pml_width); }
 
 // z-chunk length minimising (waves x (chunk + warm-up)) for ncol columns over nz planes
-static int choose_cz(int64_t ncol, int nz, int resident, double warm = 4.0) {
+static int choose_cz(int64_t ncol, int nz, int resident, double warm = 4.0, int maxcz = 1 << 30) {
   int best = nz;
   double best_cost = 1e300;
   for (int k = 1; k <= 256; ++k) {
     const int cz = (nz + k - 1) / k;
     if (cz < 8 && k > 1) break;
+    if (cz > maxcz && (nz + k) / (k + 1) >= 8) continue;
     const int64_t nch = (nz + cz - 1) / cz;
     const double waves = std::ceil((double)(ncol * nch) / std::max(1, resident));
     const double cost = waves * (cz + warm);   // warm-up planes cost ~ half a plane each
@@ -502,6 +503,8 @@ static int choose_cz(int64_t ncol, int nz, int resident, double warm = 4.0) {
   }
   return best;
 }
+
+constexpr int W25_WALL_CZ_MAX = 40;    // longest fp32 wall z-chunk (measured, C3/C2)
 
 struct ZRange { int z0, z1; };
 
@@ -707,7 +710,12 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   for (auto& z : zr) nzmax = std::max(nzmax, z.z1 - z.z0);
   if (ncol == 0 || nzmax == 0) return;
   const int resident = P->occ[ki] * P->nsm;
-  int cz = choose_cz(ncol * (int64_t)zr.size(), nzmax, resident);
+  // fp32 wall kernels: chunks of at most W25_WALL_CZ_MAX planes, so that the
+  // short wall CTAs interleave with the interior's instead of holding most SMs
+  // for one long wave (C3: 2.88 -> 2.83 ms/step; C2 keeps its one-wave 29
+  // planes; DESIGN.md §5 ablation, profiles/wallcz_r01.txt)
+  const int maxcz = (P->prec == 0 && (ki == KI_WALLX || ki == KI_WALLY)) ? W25_WALL_CZ_MAX : (1 << 30);
+  int cz = choose_cz(ncol * (int64_t)zr.size(), nzmax, resident, 4.0, maxcz);
   if (ki == KI_INNER)
     if (const char* e = getenv("WAVE25_CZ")) cz = std::max(1, std::min(nzmax, atoi(e)));
   if (is_wall(ki) && P->wall_cz > 0) cz = std::min(nzmax, P->wall_cz);
