@@ -284,7 +284,7 @@ struct wave_plan {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t side2 = nullptr;      // y walls when side2_on (WAVE25_SIDE2)
   cudaEvent_t ev_join2 = nullptr;
-  bool side2_on = false;
+  bool side2_on = false;            // set at plan creation (fp32: on)
   int wall_cz = 0;                   // WAVE25_WALL_CZ: wall chunk length (0 = auto)
   int xwall_extra = 0;               // WAVE25_XWALL_EXTRA: inner columns computed by the x-wall kernel
   bool walls_last = false;           // WAVE25_WALLS_LAST: enqueue the wall kernels after the interior
@@ -1322,6 +1322,10 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_WALL_PRIO")) P->wall_prio = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_SERIAL")) P->serial = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_XFUSE")) P->xfuse = atoi(e) != 0;
+  // fp32: x walls and y walls on two side streams, concurrently (disjoint
+  // output regions; C3 2.841 -> 2.830, C2 0.4224 -> 0.4155 ms/step,
+  // profiles/wallsched_r01.txt); WAVE25_SIDE2=0 serialises them on one
+  P->side2_on = P->prec == 0;
   if (const char* e = getenv("WAVE25_SIDE2")) P->side2_on = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));

@@ -409,7 +409,7 @@ for name in ("RAGGED", "C1"):
     {"WAVE25_WALLY_TILE": "y128x8x1"}, {"WAVE25_WALLY_TILE": "y128x16x1"},
     {"WAVE25_WALLY_TILE": "y64x8x1m3"}, {"WAVE25_XFUSE": "1"},
     {"WAVE25_FUSED": "1"}, {"WAVE25_FORK": "0", "WAVE25_PF": "0"}, {"WAVE25_CZ": "7"},
-    {"WAVE25_ORDER": "-3"}, {"WAVE25_ORDER": "2"}, {"WAVE25_MIX": "1"}, {"WAVE25_MIX": "2"},
+    {"WAVE25_ORDER": "-3"}, {"WAVE25_ORDER": "2"}, {"WAVE25_MIX": "1"}, {"WAVE25_MIX": "2"}, {"WAVE25_SIDE2": "0"}, {"WAVE25_WALL_CZ": "114"},
 ])
 def test_kernel_variants_bitwise(env):
     # every tile / scheduling variant used in the DESIGN.md ablations computes
