@@ -251,6 +251,97 @@ def roof_probe(torch):
     return gbs
 
 
+PARITY_STEPS = 12       # steps of the in-line multi-GPU parity check
+PARITY_PLANES = 8       # planes compared on each side of every slab face
+
+
+def seeded_planes(torch, z0: int, z1: int, ny: int, nx: int, seed: int, device):
+    """Global planes [z0, z1) of a seeded U(-1, 1) field, generated on the
+    device plane by plane (each plane's generator seeded by its global index),
+    so any slab or window of the same global field is bitwise identical."""
+    out = torch.empty((z1 - z0, ny, nx), dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    for k in range(z0, z1):
+        g.manual_seed(seed * 1_000_003 + k)
+        out[k - z0].uniform_(-1.0, 1.0, generator=g)
+    return out
+
+
+def multi_gpu_parity(s, plan, runner, halo, rank, world, dist, barrier):
+    """In-line correctness bit of an N>1 run.
+
+    All ranks re-initialise the wired run collectively to a seeded random
+    state (O(1) everywhere, so every face carries signal), step PARITY_STEPS
+    steps through the production exchange path, and then every face between
+    rank r-1 and rank r is checked BITWISE against a recompute on rank r by one
+    plan of the window [b - 4K - 16, b + 4K + 16) of the same global grid
+    (b = the face, K = PARITY_STEPS): the stencil reaches 4 planes per step,
+    so the window's own cut ends cannot reach the 2 x 8 planes compared.
+    Rank r-1's planes next to the face come over torch.distributed."""
+    import torch
+    from paper_2009_04619_b200.dist import SlabRunner, slab_bounds
+    from paper_2009_04619_b200.wave import WavePlan
+    import synth
+
+    K, M = PARITY_STEPS, PARITY_PLANES
+    dev = plan.device
+    off, nzl = slab_bounds(s.nz, rank, world)
+    wl = synth.wavelet_for(s, K)
+    seed_u, seed_p = 101, 202
+    u0 = seeded_planes(torch, off, off + nzl, s.ny, s.nx, seed_u, dev)
+    um1 = seeded_planes(torch, off, off + nzl, s.ny, s.nx, seed_p, dev)
+    if halo == "peer":
+        runner.reset(um1, u0, source=(*s.source, wl))
+        runner.step(K)
+    else:
+        barrier()
+        plan.set_source(*s.source, wl)
+        plan.set_state(um1, u0)
+        runner.exchange_current()
+        runner.step(K)
+    torch.cuda.synchronize()
+    del u0, um1
+    peer_ok = True
+    if halo == "peer":
+        try:
+            runner.check()
+        except Exception:
+            peer_ok = False
+    got = plan.field(0)
+    gloo = dist.get_backend() != "nccl"
+    # rank r-1 sends its last M planes to rank r
+    below = None
+    if rank < world - 1:
+        t = got[nzl - M:].contiguous()
+        dist.send(t.cpu() if gloo else t, rank + 1)
+    if rank > 0:
+        below = torch.empty((M, s.ny, s.nx), dtype=torch.float32, device="cpu" if gloo else dev)
+        dist.recv(below, rank - 1)
+    ok = True
+    if rank > 0:
+        z0, z1 = max(0, off - 4 * K - 2 * M), min(s.nz, off + 4 * K + 2 * M)
+        win = WavePlan(s.nx, s.ny, z1 - z0, s.w, s.h, s.dt, s.eta_max, nz_global=s.nz, z_offset=z0)
+        win.set_velocity(synth.velocity(s, nz_global=s.nz, z_offset=z0, nz_local=z1 - z0))
+        win.set_source(*s.source, wl)
+        win.set_state(seeded_planes(torch, z0, z1, s.ny, s.nx, seed_p, dev),
+                      seeded_planes(torch, z0, z1, s.ny, s.nx, seed_u, dev))
+        SlabRunner(win, 0, 1).step(K)          # one plan, no exchange: ghost planes stay zero
+        torch.cuda.synchronize()
+        ref = win.field(0)
+        ok = bool(torch.equal(ref[off - z0:off - z0 + M], got[:M]))
+        ok = ok and bool(torch.equal(ref[off - z0 - M:off - z0].to(below.device), below))
+        del ref
+        win.close()
+    flag = torch.tensor([1 if (ok and peer_ok) else 0], dtype=torch.int32, device="cpu" if gloo else dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    barrier()
+    return {"bitwise_faces_ok": bool(int(flag.item()) == 1), "faces": world - 1, "steps": K,
+            "planes_per_face": 2 * M, "exchange": halo,
+            "how": ("after the timed runs: collective reset to a seeded U(-1,1) state, K steps through the "
+                    "production exchange, every slab face compared bitwise with one plan of the window "
+                    "[b-4K-16, b+4K+16) recomputed on the face's upper rank")}
+
+
 def run_ours(args, rank, world, local):
     import numpy as np
     import torch
@@ -348,7 +439,7 @@ def run_ours(args, rank, world, local):
         reps.append(timed()[0])
     rep_ms = [r / args.steps for r in reps]
     value = pts_total * args.steps / (ms / 1e3) / 1e9
-    launches = plan.launches(args.steps) if world == 1 else plan.launches_per_step * args.steps
+    launches = plan.launches(args.steps) if (world == 1 or halo == "peer") else plan.launches_per_step * args.steps
 
     # ---- roofline of the dominant (interior) kernel: profiled pass -------
     roof = None
@@ -386,9 +477,16 @@ def run_ours(args, rank, world, local):
         t0 = time.perf_counter()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        plan.set_state(None, None, stream=stream)        # u^0 = u^-1 = 0
-        plan.set_velocity(Vh, stream=stream)              # H2D from pinned memory (+ vdt2 kernel)
-        plan.set_source(*s.source, wl, stream=stream)     # wavelet H2D
+        if isinstance(runner, PeerSlabRunner):
+            # a wired run is re-initialised collectively (barriers around the
+            # set_* calls, flag protocol restarted)
+            runner.reset(None, None, velocity=Vh, source=(*s.source, wl))
+        else:
+            plan.set_state(None, None, stream=stream)        # u^0 = u^-1 = 0
+            plan.set_velocity(Vh, stream=stream)              # H2D from pinned memory (+ vdt2 kernel)
+            plan.set_source(*s.source, wl, stream=stream)     # wavelet H2D
+            if runner is not None:
+                barrier()
         steps(args.steps)
         plan.read(0, out=outh, stream=stream)             # D2H of u^K
         e1.record(stream)
@@ -400,6 +498,10 @@ def run_ours(args, rank, world, local):
                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": outh.numel() * outh.element_size() / args.steps,
                "ms_total": e_ms, "api": "WavePlan.set_state/set_velocity(host)/set_source/step/read(host) "
                                          "-> libwave25.so C ABI"}
+
+    parity = None
+    if world > 1 and not args.no_parity:
+        parity = multi_gpu_parity(s, plan, runner, halo, rank, world, dist, barrier)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -422,7 +524,7 @@ def run_ours(args, rank, world, local):
                                       if halo == "peer" else "edges -> NCCL send/recv || interior, joined")},
             "hbm_gbs_at_algorithmic_bytes": value * bpp,
             "frac_of_measured_hbm": value * bpp / measured_peak()[0],
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "parity": parity,
             "clocks": clocks, "remeasured": remeasured,
             "repeats": {"n": len(rep_ms), "ms_per_step": rep_ms,
                         "ms_per_step_mean": statistics.fmean(rep_ms),
@@ -448,6 +550,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-probe", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="N>1: skip the in-line slab-face parity check")
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="N>1: weak = C5 (1024 planes per GPU), strong = C4 (the 1024^3 grid split N ways)")

@@ -59,7 +59,9 @@ typedef enum {
     WAVE_ERR_VERIFY = 3,     /* reserved for verification harnesses           */
     WAVE_ERR_CUDA = 4,       /* CUDA runtime / driver error                    */
     WAVE_ERR_ALLOC = 5,      /* host or device allocation failure              */
-    WAVE_ERR_STATE = 6       /* call out of order (e.g. step before bind)       */
+    WAVE_ERR_STATE = 6,      /* call out of order (e.g. step before bind)       */
+    WAVE_ERR_PEER = 7        /* a z-neighbour did not complete its step within
+                                the peer-wait bound (wave_peer_check)           */
 } wave_status;
 
 typedef enum { WAVE_MEM_HOST = 0, WAVE_MEM_DEVICE = 1 } wave_mem;
@@ -242,7 +244,13 @@ WAVE_API wave_status wave_set_source(wave_plan *plan, int64_t i, int64_t j, int6
 
 /* Optional initial state: u^{-1} (uprev) and u^0 (ucur), dense [nz][ny][nx]
  * fp32 in `where` memory (either may be NULL = zero).  Resets the step
- * counter to 0 and clears the halo planes. */
+ * counter to 0 and clears the halo planes.  On a peer-wired plan
+ * (wave_set_peers) it also restarts the step-flag protocol (this rank's done
+ * count, its flag words and the peer-wait error word): re-initialising a
+ * peer-wired run is COLLECTIVE -- every rank calls it after a barrier that
+ * follows its last step, then a second barrier, then wave_push_halo(1) for a
+ * non-zero state and a third barrier, before anyone steps again
+ * (dist.PeerSlabRunner.reset does exactly this). */
 WAVE_API wave_status wave_set_state(wave_plan *plan, const float *uprev, const float *ucur,
                            int32_t where, void *stream);
 
@@ -324,6 +332,17 @@ WAVE_API wave_status wave_ipc_release(void *base);
  * neighbours (system-scope fence + release stores).  No NCCL in the step;
  * replayed from CUDA graphs. */
 WAVE_API wave_status wave_step_peer(wave_plan *plan, int64_t nsteps, void *stream);
+
+/* Bound of each peer wait in device time (default 300 s, or the environment
+ * variable WAVE25_PEER_TIMEOUT_S at plan creation).  A wait that expires does
+ * not trap: it records which neighbour was late in a device error word, the
+ * run continues (its results are invalid) and wave_peer_check reports it.
+ * Re-instantiates the peer graphs (call before stepping, on every rank). */
+WAVE_API wave_status wave_set_peer_timeout(wave_plan *plan, double seconds);
+
+/* Synchronises `stream` and returns WAVE_ERR_PEER if any peer wait of this
+ * plan has expired since wave_set_peers / wave_set_state, else WAVE_OK. */
+WAVE_API wave_status wave_peer_check(wave_plan *plan, void *stream);
 
 /* Copy this slab's 4 edge planes of u^n (which = 1) or of the next buffer
  * (which = 0) into the neighbours' ghost planes (for a non-zero initial

@@ -14,9 +14,10 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libwave25.so")
 
-WAVE_OK, WAVE_ERR_CONFIG, WAVE_ERR_UNSTABLE, WAVE_ERR_VERIFY, WAVE_ERR_CUDA, WAVE_ERR_ALLOC, WAVE_ERR_STATE = range(7)
+(WAVE_OK, WAVE_ERR_CONFIG, WAVE_ERR_UNSTABLE, WAVE_ERR_VERIFY, WAVE_ERR_CUDA, WAVE_ERR_ALLOC, WAVE_ERR_STATE,
+ WAVE_ERR_PEER) = range(8)
 STATUS_NAMES = {0: "WAVE_OK", 1: "WAVE_ERR_CONFIG", 2: "WAVE_ERR_UNSTABLE", 3: "WAVE_ERR_VERIFY",
-                4: "WAVE_ERR_CUDA", 5: "WAVE_ERR_ALLOC", 6: "WAVE_ERR_STATE"}
+                4: "WAVE_ERR_CUDA", 5: "WAVE_ERR_ALLOC", 6: "WAVE_ERR_STATE", 7: "WAVE_ERR_PEER"}
 WAVE_MEM_HOST, WAVE_MEM_DEVICE = 0, 1
 WAVE_KERNEL_STREAM, WAVE_KERNEL_NAIVE, WAVE_KERNEL_TB2, WAVE_KERNEL_PAIR = 0, 1, 2, 3
 WAVE_PREC_FP32, WAVE_PREC_FP64 = 0, 1
@@ -30,7 +31,7 @@ EXPORTS = [
     "wave_step_index", "wave_get_dt", "wave_launches_per_step", "wave_kernel_points",
     "wave_step_profiled", "wave_set_peers", "wave_step_peer", "wave_push_halo",
     "wave_plan_bind_aux", "wave_launches", "wave_steps_per_launch", "wave_plan_bind_eta", "wave_set_eta",
-    "wave_ipc_export", "wave_ipc_import", "wave_ipc_release",
+    "wave_ipc_export", "wave_ipc_import", "wave_ipc_release", "wave_set_peer_timeout", "wave_peer_check",
 ]
 KERNEL_KINDS = ["interior", "xwalls", "ywalls", "source"]
 
@@ -120,6 +121,8 @@ def lib() -> ctypes.CDLL:
                 "wave_ipc_export": ([P, P, ctypes.POINTER(i64)], i32),
                 "wave_ipc_import": ([P, i64, ctypes.POINTER(P), ctypes.POINTER(P)], i32),
                 "wave_ipc_release": ([P], i32),
+                "wave_set_peer_timeout": ([P, ctypes.c_double], i32),
+                "wave_peer_check": ([P, P], i32),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)
@@ -297,6 +300,15 @@ def wave_step_peer(plan, nsteps: int, stream: int) -> None:
 
 def wave_push_halo(plan, which: int, stream: int) -> None:
     check(lib().wave_push_halo(plan, int(which), stream))
+
+
+def wave_set_peer_timeout(plan, seconds: float) -> None:
+    check(lib().wave_set_peer_timeout(plan, float(seconds)))
+
+
+def wave_peer_check(plan, stream: int) -> None:
+    """Raises WaveError(WAVE_ERR_PEER) if a peer wait of this plan expired."""
+    check(lib().wave_peer_check(plan, stream))
 
 
 def wave_ipc_export(dptr: int) -> tuple[bytes, int]:

@@ -87,16 +87,18 @@ __global__ void __launch_bounds__(128) k_naive(const T* __restrict__ u, T* __res
 
 // Source injection, PAPER.md L263 (Alg. 1) / SPEC.md L158-161: u_next[src] +=
 // inc[n], n = the device step counter (so replayed CUDA graphs stay correct).
-// `mirror` (or null): the same cell in a neighbour's ghost planes (fused halo
-// exchange), which must carry the injected value too.
+// `mlo` / `mhi` (or null): the same cell in the lower / upper neighbour's
+// ghost planes (fused halo exchange), which must carry the injected value too
+// (both, on a slab thinner than 2R planes).
 template <typename T>
 __global__ void k_source(T* __restrict__ buf, int64_t off, const T* __restrict__ inc,
-                         int64_t ninc, unsigned long long* __restrict__ dstep, T* mirror) {
+                         int64_t ninc, unsigned long long* __restrict__ dstep, T* mlo, T* mhi) {
   const unsigned long long n = *dstep;
   if (n < (unsigned long long)ninc) {
     const T v = add_rn(buf[off], inc[n]);
     buf[off] = v;
-    if (mirror) *mirror = v;
+    if (mlo) *mlo = v;
+    if (mhi) *mhi = v;
   }
   *dstep = n + 1;
 }
@@ -124,22 +126,31 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
 }
 
 // Wait until the neighbours have completed as many steps as this rank.  The
-// spin is bounded (~10 s): a mis-wired or dead neighbour traps (a CUDA error
-// on this rank) instead of hanging the GPU.
+// wait is bounded by `timeout_ns` of device time (%globaltimer): a neighbour
+// that is dead or mis-wired sets bit 0 (lower) / bit 1 (upper) of *err and the
+// wait gives up -- no trap, so the CUDA context survives; the step's results
+// are then invalid and wave_peer_check reports WAVE_ERR_PEER.  Once *err is
+// set, later waits return at once (the run is already void).
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __global__ void k_peer_wait(const unsigned long long* flags, const unsigned long long* done, int need_lo,
-                            int need_hi) {
+                            int need_hi, unsigned long long* err, unsigned long long timeout_ns) {
   const unsigned long long d = *done;
-  unsigned long long spins = 0;
-  if (need_lo)
-    while (ld_acquire_sys(flags + 0) < d) {
+  if (*err) return;
+  const unsigned long long t0 = globaltimer_ns();
+  for (int side = 0; side < 2; ++side) {
+    if (!(side == 0 ? need_lo : need_hi)) continue;
+    while (ld_acquire_sys(flags + side) < d) {
       __nanosleep(256);
-      if (++spins > (1ull << 25)) __trap();
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicOr(err, 1ull << side);
+        return;
+      }
     }
-  if (need_hi)
-    while (ld_acquire_sys(flags + 1) < d) {
-      __nanosleep(256);
-      if (++spins > (1ull << 25)) __trap();
-    }
+  }
 }
 
 // Publish "one more step completed" to both neighbours: [0] of the upper

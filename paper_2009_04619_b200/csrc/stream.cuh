@@ -825,21 +825,26 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
             if (mask & (1u << (r * NV + c))) optr[r * P.pitch + c] = vget(res[r], c);
       }
       // fused halo exchange: edge planes also go straight into the neighbour's
-      // ghost planes over the peer mapping (plane-uniform branch)
-      T* rbase = nullptr;
-      if (z < R && P.rlo) rbase = static_cast<T*>(P.rlo) + (int64_t)z * P.plane;
-      else if (z >= P.nzl - R && P.rhi) rbase = static_cast<T*>(P.rhi) + (int64_t)(z - (P.nzl - R)) * P.plane;
-      if (rbase) {
-        T* rp = rbase + (int64_t)gy * P.pitch + gx;
-        if (full) {
+      // ghost planes over the peer mapping (plane-uniform branches).  The two
+      // targets are independent: on a slab of fewer than 2R planes a plane can
+      // be an edge plane of both faces and must reach both neighbours.
 #pragma unroll
-          for (int r = 0; r < TYT; ++r) *reinterpret_cast<V*>(rp + r * P.pitch) = res[r];
-        } else {
+      for (int side = 0; side < 2; ++side) {
+        T* rbase = nullptr;
+        if (side == 0 && z < R && P.rlo) rbase = static_cast<T*>(P.rlo) + (int64_t)z * P.plane;
+        if (side == 1 && z >= P.nzl - R && P.rhi) rbase = static_cast<T*>(P.rhi) + (int64_t)(z - (P.nzl - R)) * P.plane;
+        if (rbase) {
+          T* rp = rbase + (int64_t)gy * P.pitch + gx;
+          if (full) {
 #pragma unroll
-          for (int r = 0; r < TYT; ++r)
+            for (int r = 0; r < TYT; ++r) *reinterpret_cast<V*>(rp + r * P.pitch) = res[r];
+          } else {
 #pragma unroll
-            for (int c = 0; c < NV; ++c)
-              if (mask & (1u << (r * NV + c))) rp[r * P.pitch + c] = vget(res[r], c);
+            for (int r = 0; r < TYT; ++r)
+#pragma unroll
+              for (int c = 0; c < NV; ++c)
+                if (mask & (1u << (r * NV + c))) rp[r * P.pitch + c] = vget(res[r], c);
+          }
         }
       }
       if (PAIR && role == 1) {

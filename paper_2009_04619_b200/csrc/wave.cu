@@ -316,7 +316,8 @@ struct wave_plan {
   // fused peer-store halo exchange
   bool have_peers = false;
   wave_peers peers{};
-  unsigned long long* ddone = nullptr;     // steps completed (flag protocol)
+  unsigned long long* ddone = nullptr;     // [0] steps completed (flag protocol), [1] peer-wait error bits
+  double peer_timeout_s = 300.0;           // k_peer_wait bound (WAVE25_PEER_TIMEOUT_S / wave_set_peer_timeout)
   bool remote = false;                     // enqueue with remote edge stores
   cudaGraphExec_t gexec_peer[2] = {nullptr, nullptr};
 };
@@ -554,7 +555,9 @@ static wave_status build_launches(wave_plan* P) {
     // tiles line up with the interior kernel's wide tiles
     if (w > 0) {
       const int kx = P->eta_on ? KI_WALLX_E : KI_WALLX, ky = P->eta_on ? KI_WALLY_E : KI_WALLY;
-      const int xw = w + P->xwall_extra;          // x-wall width (>= w: extra inner columns)
+      // x-wall width (>= w: extra inner columns; not with a stored eta, whose
+      // interior launch keeps the inner xy footprint)
+      const int xw = w + (P->eta_on ? 0 : P->xwall_extra);
       add_regions(P, kx, {{0, xw, 0, ny}, {nx - xw, nx, 0, ny}}, *sets[s], &P->launches[s]);
       add_regions(P, ky, {{xw, nx - xw, 0, w}, {xw, nx - xw, ny - w, ny}}, *sets[s], &P->launches[s]);
     }
@@ -916,21 +919,22 @@ static wave_status launch_source(wave_plan* P, int prv, cudaStream_t s) {
   const int64_t k = P->sk - P->d.z_offset;
   const int64_t plane = P->L.pitch_x * P->d.ny;
   const int64_t off = (k + R) * plane + P->sj * P->L.pitch_x + P->si;
-  float* mirror = nullptr;   // the source cell in a neighbour's ghost planes (fused exchange)
+  // the source cell in the neighbours' ghost planes (fused exchange); both
+  // mirrors are independent (a plane of a thin slab can be an edge of both faces)
+  float* mlo = nullptr;
+  float* mhi = nullptr;
   if (P->remote) {
     const int64_t cell = P->sj * P->L.pitch_x + P->si;
-    if (k < R && P->peers.lo_buf[prv])
-      mirror = eo(P, P->peers.lo_buf[prv], (P->peers.lo_nz + R + k) * plane + cell);
-    else if (k >= P->d.nz - R && P->peers.hi_buf[prv])
-      mirror = eo(P, P->peers.hi_buf[prv], (k - (P->d.nz - R)) * plane + cell);
+    if (k < R && P->peers.lo_buf[prv]) mlo = eo(P, P->peers.lo_buf[prv], (P->peers.lo_nz + R + k) * plane + cell);
+    if (k >= P->d.nz - R && P->peers.hi_buf[prv]) mhi = eo(P, P->peers.hi_buf[prv], (k - (P->d.nz - R)) * plane + cell);
   }
   if (P->prec)
     k_source<double><<<1, 1, 0, s>>>(reinterpret_cast<double*>(P->buf[prv]), off,
                                      static_cast<const double*>(P->inc_d), P->ninc, P->dstep,
-                                     reinterpret_cast<double*>(mirror));
+                                     reinterpret_cast<double*>(mlo), reinterpret_cast<double*>(mhi));
   else
     k_source<float><<<1, 1, 0, s>>>(P->buf[prv], off, static_cast<const float*>(P->inc_d), P->ninc, P->dstep,
-                                    mirror);
+                                    mlo, mhi);
   CK(cudaGetLastError());
   return WAVE_OK;
 }
@@ -1328,6 +1332,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   P->side2_on = P->prec == 0;
   if (const char* e = getenv("WAVE25_SIDE2")) P->side2_on = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
+  if (const char* e = getenv("WAVE25_PEER_TIMEOUT_S")) P->peer_timeout_s = std::max(1e-3, atof(e));
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
   if (const char* e = getenv("WAVE25_WALLS_LAST")) P->walls_last = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_MIX")) P->mix = atoi(e);
@@ -1601,6 +1606,8 @@ wave_status wave_set_source(wave_plan* P, int64_t i, int64_t j, int64_t k, const
   return rebuild_inc(P, s);
 }
 
+static wave_status ensure_peer_graph(wave_plan* P, int par);
+
 wave_status wave_set_state(wave_plan* P, const float* uprev, const float* ucur, int32_t where, void* stream) {
   if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
   if (!P->bound) return fail(WAVE_ERR_STATE, "bind buffers first");
@@ -1615,9 +1622,21 @@ wave_status wave_set_state(wave_plan* P, const float* uprev, const float* ucur, 
                            P->d.nx * P->esz, P->d.nx * P->esz, P->d.ny * P->d.nz, kind, s));
   }
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
+  if (P->have_peers) {
+    // restart the step-flag protocol from 0 (collective: every rank of the
+    // run re-initialises between two barriers) -- otherwise a
+    // neighbour whose count matches the stale one could pass its wait and
+    // store into ghost planes this call is about to zero
+    CK(cudaMemsetAsync(P->ddone, 0, 2 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(P->peers.my_flags, 0, 2 * sizeof(uint64_t), s));
+  }
   P->cur = 0;
   P->prv = 1;
   P->step = 0;
+  // a velocity / source change since wave_set_peers dropped the peer graphs:
+  // instantiate them now, not lazily while a neighbour's wait kernel spins
+  if (P->have_peers && P->have_vel)
+    for (int par = 0; par < 2; ++par) CKST(ensure_peer_graph(P, par));
   return WAVE_OK;
 }
 
@@ -1800,8 +1819,8 @@ wave_status wave_set_peers(wave_plan* P, const wave_peers* peers) {
   for (const void* q : {(const void*)peers->lo_buf[0], (const void*)peers->lo_buf[1], (const void*)peers->hi_buf[0],
                         (const void*)peers->hi_buf[1], (const void*)peers->lo_flags, (const void*)peers->hi_flags})
     CKST(enable_peer_for(q));
-  if (!P->ddone) CK(cudaMalloc(&P->ddone, sizeof(unsigned long long)));
-  CK(cudaMemset(P->ddone, 0, sizeof(unsigned long long)));
+  if (!P->ddone) CK(cudaMalloc(&P->ddone, 2 * sizeof(unsigned long long)));
+  CK(cudaMemset(P->ddone, 0, 2 * sizeof(unsigned long long)));
   P->peers = *peers;
   P->have_peers = true;
   // instantiate both parities' 2-step graphs now, before any peer-wait kernel
@@ -1813,7 +1832,8 @@ wave_status wave_set_peers(wave_plan* P, const wave_peers* peers) {
 static wave_status enqueue_peer_step(wave_plan* P, int cur, cudaStream_t s) {
   const bool lo = P->peers.lo_buf[0] != nullptr, hi = P->peers.hi_buf[0] != nullptr;
   using ull = unsigned long long;
-  k_peer_wait<<<1, 1, 0, s>>>(reinterpret_cast<const ull*>(P->peers.my_flags), P->ddone, lo ? 1 : 0, hi ? 1 : 0);
+  k_peer_wait<<<1, 1, 0, s>>>(reinterpret_cast<const ull*>(P->peers.my_flags), P->ddone, lo ? 1 : 0, hi ? 1 : 0,
+                              P->ddone + 1, (ull)(P->peer_timeout_s * 1e9));
   CK(cudaGetLastError());
   P->remote = true;
   wave_status st = enqueue_compute(P, 0, cur, 1 - cur, s);
@@ -1846,6 +1866,30 @@ wave_status wave_step_peer(wave_plan* P, int64_t nsteps, void* stream) {
     std::swap(P->cur, P->prv);
     P->step += 1;
   }
+  return WAVE_OK;
+}
+
+wave_status wave_set_peer_timeout(wave_plan* P, double seconds) {
+  if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
+  if (!(seconds > 0.0) || seconds > 1e6) return fail(WAVE_ERR_CONFIG, "timeout must be in (0, 1e6] s");
+  P->peer_timeout_s = seconds;
+  drop_graphs(P);                 // the bound is baked into the captured wait kernels
+  if (P->have_peers)
+    for (int par = 0; par < 2; ++par) CKST(ensure_peer_graph(P, par));
+  return WAVE_OK;
+}
+
+wave_status wave_peer_check(wave_plan* P, void* stream) {
+  if (!P) return fail(WAVE_ERR_CONFIG, "plan is NULL");
+  if (!P->ddone) return WAVE_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long e = 0;
+  CK(cudaMemcpyAsync(&e, P->ddone + 1, sizeof e, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (e)
+    return fail(WAVE_ERR_PEER, "peer wait timed out after %.3g s (%s%s neighbour did not complete its step); "
+                "the results of this run are invalid", P->peer_timeout_s, (e & 1) ? "lower" : "",
+                (e & 3) == 3 ? " and upper" : (e & 2) ? "upper" : "");
   return WAVE_OK;
 }
 
@@ -2077,6 +2121,8 @@ int32_t wave_launches_per_step(const wave_plan* P) {
 
 int64_t wave_launches(const wave_plan* P, int64_t nsteps) {
   if (!P || nsteps < 0) return -1;
+  if (P->have_peers)   // wave_step_peer: wait + all-plane compute launches + source + signal per step
+    return nsteps * ((int64_t)P->launches[0].size() + (source_active(P) ? 1 : 0) + 2);
   const int64_t single = wave_launches_per_step(P);
   if (pair_active(P)) return (nsteps / 2) * pair_l2_launches(P) + (nsteps % 2) * single;
   if (!tb2_active(P)) return single * nsteps;

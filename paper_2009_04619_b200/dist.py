@@ -230,5 +230,30 @@ class PeerSlabRunner:
         self.plan.push_halo(1)
         self._barrier()
 
+    def reset(self, uprev=None, ucur=None, velocity=None, source=None) -> None:
+        """Collective re-initialisation of the wired run (every rank calls it).
+
+        barrier (no rank is still stepping or storing into a neighbour's
+        ghost planes) -> each rank installs the new velocity / source / state;
+        wave_set_state zeroes the ghost planes and restarts the step-flag
+        protocol (done count, flag words, peer-wait error word) -> barrier
+        (every memset has landed before any neighbour writes into the ghosts)
+        -> push the new u^0 edge planes into the neighbours' ghosts -> barrier.
+        source = (i, j, k, wavelet) in global coordinates."""
+        self._barrier()
+        if velocity is not None:
+            self.plan.set_velocity(velocity)
+        if source is not None:
+            self.plan.set_source(*source)
+        self.plan.set_state(uprev, ucur)
+        self._barrier()
+        if ucur is not None:
+            self.plan.push_halo(1)
+        self._barrier()
+
+    def check(self) -> None:
+        """Raise (WAVE_ERR_PEER) if a peer wait of this rank expired."""
+        self.plan.peer_check()
+
     def step(self, n: int = 1) -> None:
         self.plan.step_peer(n)

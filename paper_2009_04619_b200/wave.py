@@ -163,6 +163,17 @@ class WavePlan:
         with torch.cuda.device(self.device):
             _abi.wave_step_peer(self._plan, n, _stream_handle(stream))
 
+    def set_peer_timeout(self, seconds: float) -> None:
+        """Bound of each peer wait (device time); an expired wait is reported
+        by peer_check, it never traps."""
+        with torch.cuda.device(self.device):
+            _abi.wave_set_peer_timeout(self._plan, seconds)
+
+    def peer_check(self, stream=None) -> None:
+        """Synchronise and raise if any peer wait expired (results invalid)."""
+        with torch.cuda.device(self.device):
+            _abi.wave_peer_check(self._plan, _stream_handle(stream))
+
     def push_halo(self, which: int = 1, stream=None) -> None:
         with torch.cuda.device(self.device):
             _abi.wave_push_halo(self._plan, which, _stream_handle(stream))

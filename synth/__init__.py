@@ -92,6 +92,11 @@ SCENARIOS = {
     "L128": Scenario("L128", 128, 128, 128, w=16, h=10.0, dt=8.888889e-4,
                      eta_max=4.0, vmodel="layered", v0=1500.0, v1=4500.0,
                      f_peak=15.0, t0=0.0666667, steps=1000),
+    # 256^3 layered x 1000 steps: the C3 recipe (V, dt, wavelet, w) on a grid
+    # the oracle finishes in seconds (SURVEY.md §8(d) oracle-timing bullet)
+    "L256": Scenario("L256", 256, 256, 256, w=16, h=10.0, dt=8.888889e-4,
+                     eta_max=4.0, vmodel="layered", v0=1500.0, v1=4500.0,
+                     f_peak=15.0, t0=0.0666667, steps=1000),
 }
 
 
