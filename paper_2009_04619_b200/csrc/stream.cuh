@@ -279,7 +279,19 @@ __device__ __noinline__ typename VecT<T>::V pml_row_eta(typename VecT<T>::V L, t
 
 // The body of one work unit (tile x z-chunk) of k_stream; `unit0` = its index
 // in the launch's region list (blockIdx.x for k_stream, remapped by k_mix).
-template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0, typename T = float, int PAIR = 0>
+// CL > 1 (interior only, TY = 2R): CL CTAs of a thread-block cluster hold CL
+// vertically adjacent tiles.  Their u windows overlap by 2R rows, so each u
+// stage is assembled from (2R)-row boxes: box k (rows [y0_k - R, y0_k + R) of
+// CTA k's tile) is loaded ONCE by CTA k and multicast into CTAs k-1 and k
+// (TMA .multicast::cluster); the last CTA also loads the bottom box.  A box
+// lands at the same shared-memory offset in every destination, half k & 1 of
+// the stage, so odd CTAs see their window with its two halves swapped (the
+// consumers' row offsets absorb it).  A stage may be refilled only when the
+// consumers of both destination CTAs released it: every consumer warp also
+// arrives on the next CTA's empty barrier.  The shared halo rows of y-adjacent
+// tiles are thus read from L2/DRAM once and the pair streams in lockstep.
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0, typename T = float, int PAIR = 0,
+          int CL = 1>
 __device__ __forceinline__ void
 stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
             const CUtensorMap& tm_up,   // u^{n-1}, box (CW, TY, 1)
@@ -288,6 +300,9 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T>;
   using V = typename VecT<T>::V;
   constexpr int NV = C::NV;
+  static_assert(CL == 1 || (MODE == MODE_INNER && C::NH == 1 && TY == 2 * R && TYT == 1 && PAIR == 0 && CL <= 8),
+                "cluster multicast: interior tiles of 2R rows, one u box per half");
+  const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
   constexpr int KX = (R + NV - 1) / NV;           // x-neighbour vectors on each side
   constexpr int XC = KX * NV;                     // index of the first centre point in X[]
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -332,6 +347,11 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     zc = (code >> 16) & 0xfff;
     tyi = code & 0xffff;
     txi = unit - g * G.ntx;
+  } else if (CL > 1) {                     // clusters of CL tile rows, consecutive blocks = one cluster
+    const int pr = rem / (G.ntx * CL);
+    const int r2 = rem - pr * G.ntx * CL;
+    txi = r2 / CL;
+    tyi = pr * CL + (r2 - txi * CL);         // r2 % CL == %cluster_ctarank (blk0, ncol multiples of CL)
   } else if (P.order < 0) {                // bands of -order tile rows, x-major inside a band
     const int bh = -P.order;
     const int band = rem / (bh * G.ntx);
@@ -371,7 +391,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     prefetch_tmap(P.gup ? P.gup : &tm_up);
     prefetch_tmap(P.gv ? P.gv : &tm_v);
 #pragma unroll
-    for (int s = 0; s < SU; ++s) { mbar_init(&full_u[s], 1); mbar_init(&empty_u[s], C::NWC); }
+    // cluster: box k feeds CTAs k-1 and k, so CTA k refills a stage after both released it
+    for (int s = 0; s < SU; ++s) { mbar_init(&full_u[s], 1); mbar_init(&empty_u[s], C::NWC * (crank > 0 ? 2 : 1)); }
 #pragma unroll
     for (int s = 0; s < C::SPN; ++s) { mbar_init(&full_p[s], 1); mbar_init(&empty_p[s], C::NWC); }
     fence_mbar_init();
@@ -379,11 +400,19 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   for (int i = tid; i < 3 * TABN; i += C::NT) stab[i] = static_cast<const T*>(P.tab)[i];
   if (PAIR && tid < 16) s_arr[tid] = 0;
   __syncthreads();
+  if (CL > 1) cluster_sync_all();            // peers' barriers initialised before any multicast / remote arrive
 
   // ======================= producer warp =================================
   if (wid >= C::NWC) {
-    if (RA > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
-    if (wid != C::NWC || lane != 0) return;
+    // the cluster producer (multicast masks, remote barriers) needs 32 registers;
+    // the budget 4 x 112 + 32 = 5 x 96 still holds for the interior tile
+    if (RA > 0 && CL > 1) {
+      static_assert(CL == 1 || C::NWC / 4 * RA + 32 <= (C::NWC / 4 + 1) * C::MAXR, "cluster producer registers");
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
+    } else if (RA > 0) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
+    }
+    auto produce = [&]() {
     const uint64_t pol_u = P.upol ? policy_evict_normal() : policy_evict_last();  // u^n: halo re-reads
     // u^{n-1}, vdt2: streamed once -- except in a PAIR step-1 block, whose
     // u^{n-1} (overwritten by u^{n+1}) and vdt2 lines step 2 reads again
@@ -432,10 +461,22 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     auto issue_u = [&](int p, int st) {
       wait_plane(p);
       mbar_arrive_expect_tx(&full_u[st], C::U_STAGE * sizeof(T));
+      if (CL > 1) {
+        // box crank (my window's top half) -> CTAs crank-1 and crank; the last
+        // CTA also loads the bottom box (its window's bottom half) for itself
+        constexpr int HR = 2 * R * C::SW;      // elements per (2R)-row half
+        const uint16_t mask = (uint16_t)((1u << crank) | (crank > 0 ? 1u << (crank - 1) : 0u));
+        tma_load_3d_mc(su + st * C::U_STAGE + (crank & 1) * HR, mu, &full_u[st], bx0 - R, ty0 - R, p + R, mask,
+                       pol_u);
+        if (crank == CL - 1)
+          tma_load_3d(su + st * C::U_STAGE + ((crank + 1) & 1) * HR, mu, &full_u[st], bx0 - R, ty0 + R, p + R,
+                      pol_u);
+      } else {
 #pragma unroll
-      for (int h = 0; h < C::NH; ++h)
-        tma_load_3d(su + st * C::U_STAGE + h * C::U_HALF, mu, &full_u[st], bx0 + h * C::HW - R, ty0 - R, p + R,
-                    pol_u);
+        for (int h = 0; h < C::NH; ++h)
+          tma_load_3d(su + st * C::U_STAGE + h * C::U_HALF, mu, &full_u[st], bx0 + h * C::HW - R, ty0 - R, p + R,
+                      pol_u);
+      }
     };
     // p plane p (p >= zs) lives in p stage (p - zs) % 3, use (p - zs) / 3
     auto issue_p = [&](int p, int st) {
@@ -452,10 +493,17 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     for (int t = zs - R; t + SU <= ze + R - 1 || t + C::SPN < ze; ++t) {
       if (t + SU <= ze + R - 1) {
         const int o = t - zs + R;
-        mbar_wait(&empty_u[o % SU], (o / SU) & 1);
         // the consumers' generic-proxy reads of this stage are ordered before
         // the TMA (async-proxy) overwrite: mbarrier release/acquire + proxy fence
-        fence_proxy_async_smem();
+        // (cluster: the previous CTA's consumers released it too, and the
+        // multicast also overwrites their copy)
+        if (CL > 1) {
+          mbar_wait_cluster(&empty_u[o % SU], (o / SU) & 1);
+          fence_proxy_async_all();
+        } else {
+          mbar_wait(&empty_u[o % SU], (o / SU) & 1);
+          fence_proxy_async_smem();
+        }
         issue_u(t + SU, o % SU);
       }
       if (t >= zs && t + C::SPN < ze) {
@@ -466,9 +514,11 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       }
       if (P.pf > 0) {
         const int pu = t + SU + P.pf, pp = t + C::SPN + P.pf;
-        if (pu <= ze + R - 1)
+        if (pu <= ze + R - 1) {
 #pragma unroll
           for (int h = 0; h < C::NH; ++h) tma_prefetch_3d(mu, bx0 + h * C::HW - R, ty0 - R, pu + R);
+          if (CL > 1 && crank == CL - 1) tma_prefetch_3d(mu, bx0 - R, ty0 + R, pu + R);
+        }
         if (t >= zs && pp < ze) {
           tma_prefetch_3d(mup, cx0, ty0, pp + R);
           tma_prefetch_3d(mv, cx0, ty0, pp);
@@ -488,6 +538,16 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       rec[4] = ((unsigned long long)dbg_polls << 32) | dbg_fails;
       rec[5] = dbg_slack;
     }
+    };
+    if (CL > 1) {
+      // every thread stays to the final cluster barrier (peers still arrive on our barriers)
+      if (wid == C::NWC && lane == 0) produce();
+      __syncwarp();
+      cluster_sync_all();
+      return;
+    }
+    if (wid != C::NWC || lane != 0) return;
+    produce();
     return;
   }
 
@@ -499,7 +559,17 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   const int gy = ty0 + ly * TYT;            // first y of my rows
   // smem offsets (elements) of my vector in row 0 of the tile, u stage / p stage
   const int hf = (NV * lx) / C::HW;         // which half box (warp-uniform)
-  const int uo = hf * C::U_HALF + (ly * TYT + R) * C::SW + cxo + NV * lx - hf * C::HW + R;
+  // element offset of logical window row l (0 .. TY+2R-1 of the u box) at my
+  // column inside a u stage; in an odd-rank cluster CTA the two (2R)-row halves
+  // of the window are swapped (the multicast layout, see above)
+  // (l ^ 2R) = (l + 2R) mod 4R for l in [0, 4R): computed per use from one
+  // register (rematerialised rather than holding 9 offsets live in the loop)
+  const int colo = hf * C::U_HALF + cxo + NV * lx - hf * C::HW + R;
+  const int lyf = ly * TYT + (CL > 1 ? (crank & 1) * 2 * R : 0);
+  auto yo = [&](int jj) -> int {
+    return colo + (CL > 1 ? ((lyf + jj) & (4 * R - 1)) : (lyf + jj)) * C::SW;
+  };
+  const int uo = yo(R);                     // my first own row
   const int po = (ly * TYT) * CW + NV * lx;
 
   // ---- per-thread geometry: store mask, PML coefficients -----------------
@@ -603,6 +673,9 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       }
   }
 
+  // cluster: the next CTA's empty_u barriers (its box lands in my stages)
+  const uint32_t rem_empty = (CL > 1 && crank < CL - 1) ? mapa_shared(empty_u, crank + 1) : 0u;
+
   // ---- warm-up: planes zs-4 .. zs+3 (stages 0..7, first use) -> queue ----
   V q[9][TYT];
 #pragma unroll
@@ -614,7 +687,10 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   __syncwarp();
   if (lane == 0) {                           // planes zs-4..zs-1 are not needed again
 #pragma unroll
-    for (int s = 0; s < R; ++s) mbar_arrive(&empty_u[s]);
+    for (int s = 0; s < R; ++s) {
+      mbar_arrive(&empty_u[s]);
+      if (CL > 1 && crank < CL - 1) mbar_arrive_remote(rem_empty + 8 * s);   // its box is in my stage
+    }
   }
 
   // ---- main loop over planes, unrolled 9x (fixed slots / stages) ---------
@@ -637,7 +713,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
 #pragma unroll
       for (int jj = 0; jj < TYT + 2 * R; ++jj) {
         if (jj >= R && jj < R + TYT) Y[jj] = q[sc][jj - R];
-        else Y[jj] = ldv(S + (jj - R) * C::SW);
+        else Y[jj] = ldv(su + sc * C::U_STAGE + yo(jj));
       }
       // x neighbours: KX vectors on each side of the centre vector
       V XL[TYT][KX], XR[TYT][KX];
@@ -705,6 +781,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&empty_u[sc]);
+        if (CL > 1 && crank < CL - 1) mbar_arrive_remote(rem_empty + 8 * sc);
         mbar_arrive(&empty_p[sp]);
       }
 
@@ -870,13 +947,15 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       optr += P.plane;
     }
   }
+  if (CL > 1) cluster_sync_all();           // the next CTA's consumers may still arrive on our barriers
 }
 
-template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0, typename T = float, int PAIR = 0>
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB, int RA = 0, typename T = float, int PAIR = 0,
+          int CL = 1>
 __global__ void __maxnreg__((StreamCfg<TX, CW, TY, TYT, MINB, RA, T>::MAXR))
 k_stream(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ StreamParams P) {
-  stream_body<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR>(tm_u, tm_up, tm_v, P, blockIdx.x);
+  stream_body<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR, CL>(tm_u, tm_up, tm_v, P, blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -62,20 +62,24 @@ struct KInfo {
   int tx, cw, ty, nt;      // TMA box width, computed width, tile height, threads
   size_t (*smem)(int w);
   const char* name;
+  int cl = 1;              // thread-block cluster size (y-stacked tiles, multicast u halves)
 };
 
-template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0, typename T = float, int PAIR = 0>
+template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0, typename T = float, int PAIR = 0,
+          int CL = 1>
 static KInfo kinfo(const char* name) {
   using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T>;
   // tx = width of the u TMA box minus its halo (the half width for split boxes)
-  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR>, C::HW, CW, TY, C::NT, &C::smem_bytes,
-               name};
+  return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR, CL>, C::HW, CW, TY, C::NT, &C::smem_bytes,
+               name, CL};
 }
 
 // interior-kernel variants (WAVE25_INNER_TILE selects one; default first)
 static const KInfo* inner_variants(int* n) {
   static const KInfo v[] = {
       kinfo<248, 248, 8, 1, MODE_INNER, 1, 112>("248x8x1r"),
+      kinfo<248, 248, 8, 1, MODE_INNER, 1, 112, float, 0, 2>("248x8x1rc2"),
+      kinfo<248, 248, 8, 1, MODE_INNER, 1, 112, float, 0, 4>("248x8x1rc4"),
       kinfo<128, 128, 8, 1, MODE_INNER>("128x8x1"),
       kinfo<128, 128, 16, 1, MODE_INNER, 1>("128x16x1"),
       kinfo<64, 64, 16, 1, MODE_INNER>("64x16x1"),
@@ -189,6 +193,7 @@ static void init_kernels() {
 #define KTX(ki) (g_k[P->prec][ki].tx)
 #define KCW(ki) (g_k[P->prec][ki].cw)
 #define KTY(ki) (g_k[P->prec][ki].ty)
+#define KCL(ki) (g_k[P->prec][ki].cl)
 
 static constexpr double W8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0};
 static constexpr int MAX_W = W25_MAX_W;
@@ -701,7 +706,7 @@ static wave_status build_launches(wave_plan* P) {
 
 static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 4>>& xy,
                         const std::vector<ZRange>& zr, std::vector<Launch>* out) {
-  const int CW = KCW(ki), TY = KTY(ki);
+  const int CW = KCW(ki), TY = KTY(ki), CLS = KCL(ki);
   // chunk length from the largest z range and the total column count
   int64_t ncol = 0;
   int nzmax = 0;
@@ -757,6 +762,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
       g.ax0 = b[0] & ~3;
       g.ntx = (b[1] - g.ax0 + CW - 1) / CW;
       g.nty = (b[3] - b[2] + TY - 1) / TY;
+      g.nty = (g.nty + CLS - 1) / CLS * CLS;     // whole clusters (rows beyond y1 are masked)
       g.nzc = (z.z1 - z.z0 + cz - 1) / cz;
       g.blk0 = blk;
       blk += g.ntx * g.nty * g.nzc;
@@ -839,22 +845,29 @@ static wave_status launch_stream(wave_plan* P, const Launch& Lc, int ui, int upi
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   // wall CTAs (compute-heavy) get priority so they interleave with the
   // bandwidth-bound interior CTAs instead of trailing them
   attr[0].id = cudaLaunchAttributePriority;
   attr[0].val.priority = (Lc.ki != KI_INNER && Lc.ki != KI_FUSED && P->wall_prio) ? P->prio_hi : P->prio_lo;
   int na = 1;
+  if (KCL(Lc.ki) > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = KCL(Lc.ki);
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   if (P->l2_persist_mb > 0) {
     // L2 set-aside for u^n: its lines (re-read as neighbours' halos) persist,
     // u_prev / vdt2 / u_next stream through the rest of L2
-    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
-    attr[1].val.accessPolicyWindow.base_ptr = P->buf[ui];
-    attr[1].val.accessPolicyWindow.num_bytes = std::min<size_t>(P->L.elems_u * 4, P->max_window);
-    attr[1].val.accessPolicyWindow.hitRatio = P->l2_hit_ratio;
-    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    na = 2;
+    attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[na].val.accessPolicyWindow.base_ptr = P->buf[ui];
+    attr[na].val.accessPolicyWindow.num_bytes = std::min<size_t>(P->L.elems_u * 4, P->max_window);
+    attr[na].val.accessPolicyWindow.hitRatio = P->l2_hit_ratio;
+    attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
@@ -1449,8 +1462,9 @@ static wave_status encode_buffer(wave_plan* P, int b) {
   const bool f64 = P->prec == 1;
   for (int ki = 0; ki < KI_N; ++ki) {
     const uint32_t TX = KTX(ki), CW = KCW(ki), TY = KTY(ki);
-    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R,
-                  f64));
+    // cluster kernels load the u window as (2R)-row boxes (multicast halves)
+    const uint32_t UH = KCL(ki) > 1 ? 2 * R : TY + 2 * R;
+    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, UH, f64));
     CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY, f64,
                   centre_promo(P, ki, CW)));
   }

@@ -115,6 +115,8 @@ def reference(scen, phases):
     (("RAGGED", {}), [0, 20, 25, 53], [(19, 71)]),
     # 3 ranks, middle slab of exactly R planes (every plane an edge of both faces)
     (("RAGGED", {}), [0, 24, 28, 53], [(15, 73)]),
+    # 4 ranks, two adjacent R-plane slabs (a thin slab's neighbour is thin too)
+    (("RAGGED", {}), [0, 24, 28, 32, 53], [(13, 77)]),
     # 4 ranks, strong-scaling geometry: thin slabs, the z-PML (w=5) only on the
     # end ranks, the source on plane 20 = the first plane of a 7-plane slab (an
     # edge plane of both of its faces: mirrored into both neighbours)
@@ -137,10 +139,16 @@ def test_peer_reset_mid_run_bitwise():
     assert np.array_equal(got, ref) and np.array_equal(gotp, refp)
 
 
-@pytest.mark.parametrize("bounds", [[0, 20, 25, 53], [0, 24, 28, 32, 53]])
+@pytest.mark.parametrize("bounds", [[0, 20, 25, 53]])
 def test_peer_store_thin_slabs_one_process_bitwise(bounds):
-    # the same thin-slab cases with all slabs in one process (device pointers,
-    # each slab on its own stream)
+    # a thin-slab case with all slabs in one process (device pointers, each
+    # slab on its own stream).  Kept to <= 3 slabs: every plan drives 3 streams
+    # (interior + two wall side streams), and once more streams than the
+    # device's hardware work queues (CUDA_DEVICE_MAX_CONNECTIONS, default 8)
+    # are busy, two plans' streams can share a queue, so one plan's spinning
+    # peer-wait kernel can block its neighbour's wall kernels behind it -- a
+    # false dependency of the single-process test harness only (one process
+    # per GPU in production; the 4-slab cases run as 4 processes above)
     from paper_2009_04619_b200.wave import WavePlan
     s = synth.scenario("RAGGED")
     sh = (s.nz, s.ny, s.nx)
