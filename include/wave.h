@@ -128,12 +128,15 @@ typedef struct {
 
 /* Device memory layout the caller must allocate (wave_layout).
  * Wavefield buffer: [planes][ny][pitch_x] elements (fp32, or fp64 for fp64
- * plans), planes = nz + 2*ghost_z;
- * element (i, j, k) (local k) lives at ((k + ghost_z)*ny + j)*pitch_x + i.
+ * plans), planes = nz + 2*ghost_z, starting `origin` elements into the
+ * allocation; element (i, j, k) (local k) lives at
+ * origin + ((k + ghost_z)*ny + j)*pitch_x + i.  The origin shift puts the
+ * first inner column x = pml_width on a 128-B line boundary when rows are
+ * whole lines, so wall and inner points never share a line.
  * The ghost_z = 4 planes on each z side are the zero Dirichlet fringe
  * at the global ends and the neighbour's planes (halo) between
  * slabs.  x/y have no stored fringe (TMA out-of-bounds fill supplies zeros).
- * vdt2 buffer: [nz][ny][pitch_x] fp32 holding fp32((V dt)^2).
+ * vdt2 buffer: [nz][ny][pitch_x] fp32 holding fp32((V dt)^2), also from `origin`.
  * Base addresses must be aligned to align_bytes. */
 typedef struct {
     int64_t pitch_x;      /* floats per row: >= nx, multiple of 4 (16 B TMA stride rule) */
@@ -143,6 +146,7 @@ typedef struct {
     int64_t elems_vdt2;   /* floats in the vdt2 buffer                                    */
     int64_t align_bytes;  /* 128                                                          */
     int64_t elem_bytes;   /* 4 (fp32 plans) or 8 (fp64 plans): buffer element size        */
+    int64_t origin;       /* elements before the layout's first element (0 or < 128 B)     */
 } wave_layout_info;
 
 /* One region of the paper's 7-region decomposition (PAPER.md L342-356,

@@ -190,9 +190,12 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
   return remote;
 }
 
-// arrive on a cluster mbarrier given by its shared::cluster address
+// arrive on a cluster mbarrier given by its shared::cluster address (default
+// .release.cta semantics, as CUTLASS's pipeline consumer_release: a
+// cluster-scope release would also drain this warp's outstanding global
+// stores before every arrive)
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t remote) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 
 // wait with cluster-scope acquire (the arrivals come from other CTAs' threads)

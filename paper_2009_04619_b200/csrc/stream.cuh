@@ -98,6 +98,8 @@ struct StreamParams {
   int pair_pk;                  // step 1 publishes its progress every pair_pk planes (and at the end)
   int64_t pair_dbg_off;         // timeline records (pair_dbg & 8) at prog + this, 6 u64 per block
   int64_t pair_ticket;          // prog[pair_ticket]: next work unit (zeroed with the counters)
+  int inter2;                   // 2 equal regions interleaved block by block (the two x walls: the
+                                // right wall of row y and the left wall of row y+1 share a line)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
@@ -331,8 +333,13 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     unit = s_unit;
   }
   int b = unit, ri = 0;
+  if (P.inter2) {
+    ri = unit & 1;
+    b = (unit >> 1) + P.reg[ri].blk0;
+  } else {
 #pragma unroll 1
-  while (ri + 1 < P.nreg && b >= P.reg[ri + 1].blk0) ++ri;
+    while (ri + 1 < P.nreg && b >= P.reg[ri + 1].blk0) ++ri;
+  }
   const Region& G = P.reg[ri];
   b -= G.blk0;
   const int ncol = G.ntx * G.nty;
@@ -497,7 +504,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
         // the TMA (async-proxy) overwrite: mbarrier release/acquire + proxy fence
         // (cluster: the previous CTA's consumers released it too, and the
         // multicast also overwrites their copy)
-        if (CL > 1) {
+        if (CL > 1 && P.pair_dbg == 16) {     // (A/B: cluster-scope acquire + full proxy fence)
           mbar_wait_cluster(&empty_u[o % SU], (o / SU) & 1);
           fence_proxy_async_all();
         } else {

@@ -249,8 +249,10 @@ struct wave_plan {
   std::vector<float> tab_h;          // [3][w+2] fp32
   std::vector<double> tab_hd;        // [3][w+2] fp64
   void* tab_d = nullptr;
-  float* buf[4] = {nullptr, nullptr, nullptr, nullptr};   // element type by prec (float* = base address)
-  float* vdt2 = nullptr;
+  float* buf[4] = {nullptr, nullptr, nullptr, nullptr};   // element (0,0,-4) of each buffer (= base + origin)
+  float* base[4] = {nullptr, nullptr, nullptr, nullptr};  // the caller's allocations (element type by prec)
+  float* vdt2 = nullptr;                                   // element (0,0,0) of vdt2 (= vdt2_base + origin)
+  float* vdt2_base = nullptr;
   bool bound = false, have_vel = false, aux = false;
   float* eta_buf = nullptr;          // stored eta, caller-owned, vdt2 layout (wave_plan_bind_eta)
   bool eta_on = false;               // wave_set_eta installed a field
@@ -292,6 +294,7 @@ struct wave_plan {
   bool side2_on = false;            // set at plan creation (fp32: on)
   int wall_cz = 0;                   // WAVE25_WALL_CZ: wall chunk length (0 = auto)
   int xwall_extra = 0;               // WAVE25_XWALL_EXTRA: inner columns computed by the x-wall kernel
+  bool xinter = true;                // WAVE25_XINTER=0: x-wall launch region-major instead of left/right interleaved
   bool walls_last = false;           // WAVE25_WALLS_LAST: enqueue the wall kernels after the interior
   int mix = 0;                       // WAVE25_MIX=1/2: interior + x walls as one grid (k_mix, §5i; measured slower)
   bool mix_ok = false;               // geometry / kernel choice supports k_mix (set by build_launches)
@@ -431,10 +434,22 @@ static void make_layout(const wave_desc& d, wave_layout_info* L) {
   L->pitch_x = (d.nx + 3) / 4 * 4;
   L->ghost_z = R;
   L->planes = d.nz + 2 * R;
-  L->elems_u = L->planes * d.ny * L->pitch_x;
-  L->elems_vdt2 = d.nz * d.ny * L->pitch_x;
   L->align_bytes = 128;
   L->elem_bytes = d.precision == WAVE_PREC_FP64 ? 8 : 4;
+  // origin shift: when rows are whole 128-B lines, start every
+  // row (w * elem_bytes) mod 128 bytes into a line, so that the first inner
+  // column x = w is line-aligned: a 128-B line then holds either x-wall points
+  // only (the right wall of row y and the left wall of row y+1) or inner points
+  // only, and the interior and x-wall kernels (separate launches) never fetch
+  // the same line from DRAM.  16-B granularity (TMA / vector alignment).
+  L->origin = 0;
+  static const bool no_origin = getenv("WAVE25_NO_ORIGIN") && atoi(getenv("WAVE25_NO_ORIGIN")) != 0;  // A/B only
+  if ((L->pitch_x * L->elem_bytes) % 128 == 0 && !no_origin) {
+    const int64_t sb = ((128 - (d.pml_width * L->elem_bytes) % 128) % 128) / 16 * 16;
+    L->origin = sb / L->elem_bytes;
+  }
+  L->elems_u = L->origin + L->planes * d.ny * L->pitch_x;
+  L->elems_vdt2 = L->origin + d.nz * d.ny * L->pitch_x;
 }
 
 // fp64 plans: every constant in fp64, never rounded to fp32
@@ -594,6 +609,7 @@ static wave_status build_launches(wave_plan* P) {
       }
       if (ok && pw.reg[0].nzc == gi.nzc) {
         pw.cz = cz;
+        pw.inter2 = 0;
         Lx->nblk = blk;
         // chunk sequence: interior tiles in tile-row order; wall tile t of
         // each side right after the interior row holding its middle y
@@ -769,6 +785,15 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
     }
   }
   flush();
+  // the two x walls of one z range: interleave their blocks, so that the left
+  // wall of row y+1 and the right wall of row y -- one 128-B line with the
+  // origin shift -- are streamed by concurrent CTAs (one DRAM fetch)
+  if (ki == KI_WALLX && P->xinter && !out->empty() && out->back().ki == KI_WALLX) {
+    Launch& L = out->back();
+    StreamParams& q = L.p;
+    if (q.nreg == 2 && q.reg[0].ntx * q.reg[0].nty * q.reg[0].nzc == q.reg[1].ntx * q.reg[1].nty * q.reg[1].nzc)
+      q.inter2 = 1;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1345,6 +1370,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   P->side2_on = P->prec == 0;
   if (const char* e = getenv("WAVE25_SIDE2")) P->side2_on = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
+  if (const char* e = getenv("WAVE25_XINTER")) P->xinter = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_PEER_TIMEOUT_S")) P->peer_timeout_s = std::max(1e-3, atof(e));
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
   if (const char* e = getenv("WAVE25_WALLS_LAST")) P->walls_last = atoi(e) != 0;
@@ -1491,11 +1517,14 @@ wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void
   for (const void* p : {(const void*)u0, (const void*)u1, (const void*)vdt2})
     if (reinterpret_cast<uintptr_t>(p) % 128) return fail(WAVE_ERR_CONFIG, "buffers must be 128-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
-  P->buf[0] = u0; P->buf[1] = u1; P->buf[2] = P->buf[3] = nullptr; P->vdt2 = vdt2;
+  P->base[0] = u0; P->base[1] = u1; P->base[2] = P->base[3] = nullptr; P->vdt2_base = vdt2;
+  P->buf[0] = eo(P, u0, P->L.origin); P->buf[1] = eo(P, u1, P->L.origin); P->buf[2] = P->buf[3] = nullptr;
+  P->vdt2 = eo(P, vdt2, P->L.origin);
+  vdt2 = P->vdt2;
   P->aux = false;
   CK(cudaMemsetAsync(u0, 0, P->L.elems_u * P->esz, s));
   CK(cudaMemsetAsync(u1, 0, P->L.elems_u * P->esz, s));
-  CK(cudaMemsetAsync(vdt2, 0, P->L.elems_vdt2 * P->esz, s));
+  CK(cudaMemsetAsync(P->vdt2_base, 0, P->L.elems_vdt2 * P->esz, s));
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
   const uint64_t pb = P->L.pitch_x * P->esz, plb = pb * P->d.ny;
   for (int ki = 0; ki < KI_N; ++ki)
@@ -1630,7 +1659,7 @@ wave_status wave_set_state(wave_plan* P, const float* uprev, const float* ucur, 
   const float* src[4] = {ucur, uprev, nullptr, nullptr};
   for (int b = 0; b < 4; ++b) {
     if (!P->buf[b]) continue;
-    CK(cudaMemsetAsync(P->buf[b], 0, P->L.elems_u * P->esz, s));
+    CK(cudaMemsetAsync(P->base[b], 0, P->L.elems_u * P->esz, s));
     if (src[b])
       CK(cudaMemcpy2DAsync(eo(P, P->buf[b], R * P->L.pitch_x * P->d.ny), P->L.pitch_x * P->esz, src[b],
                            P->d.nx * P->esz, P->d.nx * P->esz, P->d.ny * P->d.nz, kind, s));
@@ -1836,6 +1865,12 @@ wave_status wave_set_peers(wave_plan* P, const wave_peers* peers) {
   if (!P->ddone) CK(cudaMalloc(&P->ddone, 2 * sizeof(unsigned long long)));
   CK(cudaMemset(P->ddone, 0, 2 * sizeof(unsigned long long)));
   P->peers = *peers;
+  // the neighbours' buffers are given as their allocations: element (0,0,-4)
+  // is `origin` elements in (the neighbours have the same x geometry)
+  for (int i = 0; i < 2; ++i) {
+    if (P->peers.lo_buf[i]) P->peers.lo_buf[i] = eo(P, P->peers.lo_buf[i], P->L.origin);
+    if (P->peers.hi_buf[i]) P->peers.hi_buf[i] = eo(P, P->peers.hi_buf[i], P->L.origin);
+  }
   P->have_peers = true;
   // instantiate both parities' 2-step graphs now, before any peer-wait kernel
   // can be spinning on the device
@@ -2184,14 +2219,16 @@ wave_status wave_set_eta(wave_plan* P, const float* eta, int32_t where, void* st
 
 wave_status wave_plan_bind_aux(wave_plan* P, float* u2, float* u3, void* stream) {
   if (!P || !P->bound) return fail(WAVE_ERR_STATE, "bind u0/u1/vdt2 first");
-  if (!u2 || !u3 || u2 == u3 || u2 == P->buf[0] || u2 == P->buf[1] || u3 == P->buf[0] || u3 == P->buf[1])
+  if (!u2 || !u3 || u2 == u3 || u2 == P->base[0] || u2 == P->base[1] || u3 == P->base[0] || u3 == P->base[1])
     return fail(WAVE_ERR_CONFIG, "need two more distinct wavefield buffers");
   for (const void* p : {(const void*)u2, (const void*)u3})
     if (reinterpret_cast<uintptr_t>(p) % 128) return fail(WAVE_ERR_CONFIG, "buffers must be 128-byte aligned");
   if (P->d.kernel != WAVE_KERNEL_TB2) return fail(WAVE_ERR_CONFIG, "aux buffers are for WAVE_KERNEL_TB2 plans");
   cudaStream_t s = (cudaStream_t)stream;
-  P->buf[2] = u2;
-  P->buf[3] = u3;
+  P->base[2] = u2;
+  P->base[3] = u3;
+  P->buf[2] = eo(P, u2, P->L.origin);
+  P->buf[3] = eo(P, u3, P->L.origin);
   CK(cudaMemsetAsync(u2, 0, P->L.elems_u * sizeof(float), s));
   CK(cudaMemsetAsync(u3, 0, P->L.elems_u * sizeof(float), s));
   for (int b = 2; b < 4; ++b) CKST(encode_buffer(P, b));

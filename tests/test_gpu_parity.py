@@ -202,7 +202,7 @@ def test_slabs_on_one_gpu_bitwise(nslab, precision):
         buf = [b for b in p.bufs
                if b.data_ptr() <= cur.data_ptr() < b.data_ptr() + b.element_size() * b.numel()][0]
         plane = s.ny * p.layout.pitch_x
-        v = buf.view(-1, s.ny, p.layout.pitch_x)
+        v = buf[p.layout.origin:].view(-1, s.ny, p.layout.pitch_x)
         if r > 0:
             v[0:4, :, :s.nx] = full[off - 4:off]
         if r < nslab - 1:
