@@ -13,6 +13,10 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libwave25.so")
+# A/B measurement builds only (e.g. the scalar-arithmetic build of
+# scripts/build_variant.sh): another in-tree library of the same ABI
+if os.environ.get("WAVE25_LIB"):
+    LIB_PATH = os.path.join(HERE, os.path.basename(os.environ["WAVE25_LIB"]))
 
 (WAVE_OK, WAVE_ERR_CONFIG, WAVE_ERR_UNSTABLE, WAVE_ERR_VERIFY, WAVE_ERR_CUDA, WAVE_ERR_ALLOC, WAVE_ERR_STATE,
  WAVE_ERR_PEER) = range(8)

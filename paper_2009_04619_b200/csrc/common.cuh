@@ -82,6 +82,48 @@ __device__ __forceinline__ T upd_pml(T L, T g, T c, T up, T v, T A, T B) {
   return num == T(0) ? num : div_rn(num, B);
 }
 
+// ---------------------------------------------------------------------------
+// Packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2: two IEEE fp32 operations
+// per instruction, each lane rounded exactly as the scalar instruction -- the
+// results are bitwise those of add_rn / mul_rn / fma_rn element by element).
+// A pair lives in one 64-bit register pair {lo, hi}.
+// ---------------------------------------------------------------------------
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_bcast(float a) { return f2_pack(a, a); }
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b) {
+  f2_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+  f2_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+  f2_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+// upd_inner on a pair: (2u - up) + v L; 2u is exact, so (u + u) - up rounds
+// exactly as fma(2, u, -up)
+__device__ __forceinline__ f2_t f2_upd_inner(f2_t L, f2_t c, f2_t up, f2_t v) {
+  return f2_fma(v, L, f2_sub(f2_add(c, c), up));
+}
+
 // 16-byte vector of the precision: 4 floats or 2 doubles per lane
 template <typename T> struct VecT;
 template <> struct VecT<float> { using V = float4; static constexpr int N = 4; };

@@ -51,6 +51,9 @@ struct Region {
 constexpr int MAX_REGIONS = 4;
 constexpr int SU = 9;           // u ring stages  (= 2R+1)
 constexpr int SP = 3;           // u_prev/vdt2 ring stages of the TB2 kernel (divides 9)
+#ifndef W25_PACKED
+#define W25_PACKED 1            // fp32 Laplacian on packed pairs (FFMA2); -DW25_PACKED=0 for the scalar A/B build
+#endif
 #ifndef W25_SP_MAX
 #define W25_SP_MAX 4            // deepest u_prev/vdt2 ring k_stream may use (A/B builds: -DW25_SP_MAX=3)
 #endif
@@ -100,6 +103,9 @@ struct StreamParams {
   int64_t pair_ticket;          // prog[pair_ticket]: next work unit (zeroed with the counters)
   int inter2;                   // 2 equal regions interleaved block by block (the two x walls: the
                                 // right wall of row y and the left wall of row y+1 share a line)
+  // stored eta through the u_prev/vdt2 ring (MODE_WALL_ETA): [nz][ny][pitch]
+  // fp32, box (CW + 8) x (TY + 2), out-of-range cells (eta = 0) zero-filled
+  alignas(64) CUtensorMap tm_eta;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
@@ -130,7 +136,7 @@ template <> __device__ __forceinline__ const CoefT<double>& coef_of<double>(cons
 // that gives its registers back (setmaxnreg.dec to 24) so that the consumer
 // warpgroups can raise theirs to RA (setmaxnreg.inc) -- Blackwell/Hopper
 // warp-specialised register reallocation.  Needs NWC % 4 == 0.
-template <int TX, int CW, int TY, int TYT, int MINB = 2, int RA = 0, typename T = float>
+template <int TX, int CW, int TY, int TYT, int MINB = 2, int RA = 0, typename T = float, int ETA = 0>
 struct StreamCfg {
   static constexpr int NV = VecT<T>::N;                     // x points per lane vector
   static constexpr int LXW = (CW / NV) < 8 ? (CW / NV) : 8; // vector lanes per warp row
@@ -155,19 +161,25 @@ struct StreamCfg {
   static constexpr int U_HALF = SW * SH;
   static constexpr int U_STAGE = NH * U_HALF;               // elements per u stage
   static constexpr int P_STAGE = CW * TY;                   // elements per u_prev / vdt2 stage
+  // stored-eta kernels (ETA): an fp32 eta box of (CW + 8) x (TY + 2) per u_prev
+  // stage -- the tile with a 1-cell y halo and a 4-cell (16-B) x halo
+  static constexpr int EW = CW + 8;
+  static constexpr int E_STAGE = ETA ? (EW * (TY + 2) + 31) / 32 * 32 : 0;  // floats (stages 128-B aligned)
   // u_prev / vdt2 ring depth: as deep as shared memory allows (3..W25_SP_MAX
   // stages), so more of those two streams is in flight per SM
   static constexpr int fits_(int n) {
-    return (SU * U_STAGE + 2 * n * P_STAGE) * (int)sizeof(T) + 2 * (SU + n) * 8 +
+    return (SU * U_STAGE + 2 * n * P_STAGE) * (int)sizeof(T) + n * E_STAGE * 4 + 2 * (SU + n) * 8 +
                3 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
   }
   static constexpr int SPN = (W25_SP_MAX >= 5 && fits_(5)) ? 5 : (W25_SP_MAX >= 4 && fits_(4)) ? 4 : 3;
-  static constexpr int BAR_OFF = (SU * U_STAGE + 2 * SPN * P_STAGE) * (int)sizeof(T);  // bytes
+  static constexpr int E_OFF = (SU * U_STAGE + 2 * SPN * P_STAGE) * (int)sizeof(T);    // bytes (eta ring)
+  static constexpr int BAR_OFF = E_OFF + SPN * E_STAGE * 4;                             // bytes
   static constexpr int TAB_OFF = BAR_OFF + 2 * (SU + SPN) * 8;
   static size_t smem_bytes(int w) { return TAB_OFF + 3 * (w + 2) * sizeof(T); }
   static_assert(CW % 4 == 0 && CW <= TX && TX % 4 == 0, "tile widths");
   static_assert(32 % LXW == 0 && (TY / TYT) % LYW == 0 && TY % TYT == 0, "warp tiling");
-  static_assert((U_HALF * sizeof(T)) % 128 == 0 && (P_STAGE * sizeof(T)) % 128 == 0, "TMA smem alignment");
+  static_assert((U_HALF * sizeof(T)) % 128 == 0 && (P_STAGE * sizeof(T)) % 128 == 0 && (E_STAGE * 4) % 128 == 0,
+                "TMA smem alignment");
   static_assert(NH == 1 || (CW == TX && TX % 8 == 0 && (HW / NV) % LXW == 0), "half tiles must be warp-aligned");
   static_assert(RA == 0 || (MINB == 1 && NWC % 4 == 0 && RA % 8 == 0 &&
                             NWC / 4 * RA + 24 <= (NWC / 4 + 1) * MAXR), "register reallocation budget");
@@ -242,38 +254,34 @@ __device__ __noinline__ typename VecT<T>::V pml_row_call(typename VecT<T>::V L, 
   return vmake<T>(res);
 }
 
-// Stored-eta PML path for one vector row (reading R16): eta on
-// the 7-point star read from the given field (0 outside the domain), A/B =
-// 1 -+ eta dt from the point's own value computed in fp64 and rounded once;
-// points with d = 0 (geometric) take the inner formula.
+// Stored-eta PML path for one vector row (reading R16), with
+// the eta star already staged (the eta box of the u_prev/vdt2 ring):
+// e0 / exm / exp / eym / eyp / ezm / ezp are eta at the point and its 6
+// neighbours (0 outside the domain, by TMA zero fill); A/B = 1 -+ eta dt from
+// the point's own value computed in fp64 and rounded once; points with d = 0
+// (geometric) take the inner formula.
 template <typename T>
-__device__ __noinline__ typename VecT<T>::V pml_row_eta(typename VecT<T>::V L, typename VecT<T>::V C,
-                                                        typename VecT<T>::V up, typename VecT<T>::V v,
-                                                        typename VecT<T>::V xp, typename VecT<T>::V xm,
-                                                        typename VecT<T>::V yp, typename VecT<T>::V ym,
-                                                        typename VecT<T>::V zp, typename VecT<T>::V zm, int gx,
-                                                        int gy, int z, PmlGeoT<T> G, const float* __restrict__ eta,
-                                                        int64_t pitch, int nzl, double dt) {
+__device__ __forceinline__ typename VecT<T>::V pml_row_eta_s(
+    typename VecT<T>::V L, typename VecT<T>::V C, typename VecT<T>::V up, typename VecT<T>::V v,
+    typename VecT<T>::V xp, typename VecT<T>::V xm, typename VecT<T>::V yp, typename VecT<T>::V ym,
+    typename VecT<T>::V zp, typename VecT<T>::V zm, int gx, int gy, int z, PmlGeoT<T> G, const float* e0,
+    const float* exm, const float* exp_, const float* eym, const float* eyp, const float* ezm, const float* ezp,
+    double dt) {
   constexpr int NV = VecT<T>::N;
-  auto E = [&](int x, int y, int zz) -> T {
-    if (x < 0 || x >= G.nx || y < 0 || y >= G.ny || zz < 0 || zz >= nzl) return T(0);
-    return (T)__ldg(eta + ((int64_t)zz * G.ny + y) * pitch + x);
-  };
   const int dy = dist1(gy, G.ny, G.w), dz = dist1(z, G.nzg, G.w);
   T res[NV];
 #pragma unroll
   for (int c = 0; c < NV; ++c) {
-    const int x = gx + c;
-    const int d = max(max(dist1(x, G.nx, G.w), dy), dz);
+    const int d = max(max(dist1(gx + c, G.nx, G.w), dy), dz);
     const T uc = vget(C, c), upc = vget(up, c), vc = vget(v, c), Lc = vget(L, c);
     if (d == 0) {
       res[c] = upd_inner(Lc, uc, upc, vc);
     } else {
-      const T g = add_rn(add_rn(gterm(E(x + 1, gy, z), E(x - 1, gy, z), vget(xp, c), vget(xm, c), G.i2hx),
-                                gterm(E(x, gy + 1, z), E(x, gy - 1, z), vget(yp, c), vget(ym, c), G.i2hy)),
-                         gterm(E(x, gy, z + 1), E(x, gy, z - 1), vget(zp, c), vget(zm, c), G.i2hz));
-      const double e0 = (double)E(x, gy, z);
-      res[c] = upd_pml(Lc, g, uc, upc, vc, (T)(1.0 - e0 * dt), (T)(1.0 + e0 * dt));
+      const T g = add_rn(add_rn(gterm((T)exp_[c], (T)exm[c], vget(xp, c), vget(xm, c), G.i2hx),
+                                gterm((T)eyp[c], (T)eym[c], vget(yp, c), vget(ym, c), G.i2hy)),
+                         gterm((T)ezp[c], (T)ezm[c], vget(zp, c), vget(zm, c), G.i2hz));
+      const double ee = (double)e0[c];
+      res[c] = upd_pml(Lc, g, uc, upc, vc, (T)(1.0 - ee * dt), (T)(1.0 + ee * dt));
     }
   }
   return vmake<T>(res);
@@ -299,7 +307,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
             const CUtensorMap& tm_up,   // u^{n-1}, box (CW, TY, 1)
             const CUtensorMap& tm_v,    // vdt2, box (CW, TY, 1)
             const StreamParams& P, const int unit0) {
-  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T>;
+  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T, MODE == MODE_WALL_ETA>;
   using V = typename VecT<T>::V;
   constexpr int NV = C::NV;
   static_assert(CL == 1 || (MODE == MODE_INNER && C::NH == 1 && TY == 2 * R && TYT == 1 && PAIR == 0 && CL <= 8),
@@ -311,6 +319,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   T* su = reinterpret_cast<T*>(smem_raw);
   T* sup = su + SU * C::U_STAGE;
   T* sv = sup + C::SPN * C::P_STAGE;
+  float* se = reinterpret_cast<float*>(smem_raw + C::E_OFF);   // stored-eta ring (MODE_WALL_ETA)
   uint64_t* full_u = reinterpret_cast<uint64_t*>(smem_raw + C::BAR_OFF);
   uint64_t* empty_u = full_u + SU;
   uint64_t* full_p = empty_u + SU;
@@ -487,9 +496,10 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     };
     // p plane p (p >= zs) lives in p stage (p - zs) % 3, use (p - zs) / 3
     auto issue_p = [&](int p, int st) {
-      mbar_arrive_expect_tx(&full_p[st], 2 * C::P_STAGE * sizeof(T));
+      mbar_arrive_expect_tx(&full_p[st], 2 * C::P_STAGE * sizeof(T) + C::E_STAGE * 4);
       tma_load_3d(sup + st * C::P_STAGE, mup, &full_p[st], cx0, ty0, p + R, pol_s);
       tma_load_3d(sv + st * C::P_STAGE, mv, &full_p[st], cx0, ty0, p, pol_s);
+      if (MODE == MODE_WALL_ETA) tma_load_3d(se + st * C::E_STAGE, &P.tm_eta, &full_p[st], cx0 - 4, ty0 - 1, p, pol_s);
     };
     for (int s = 0; s < SU; ++s)
       if (zs - R + s <= ze + R - 1) issue_u(zs - R + s, s);      // planes zs-4 .. zs+4
@@ -683,6 +693,20 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   // cluster: the next CTA's empty_u barriers (its box lands in my stages)
   const uint32_t rem_empty = (CL > 1 && crank < CL - 1) ? mapa_shared(empty_u, crank + 1) : 0u;
 
+  // stored eta staged through the u_prev/vdt2 ring: my points' eta of the
+  // previous plane is carried in registers (its stage is already released)
+  constexpr bool ES = MODE == MODE_WALL_ETA;
+  float eprev[ES ? TYT : 1][ES ? NV : 1];
+  if (ES) {
+#pragma unroll
+    for (int r = 0; r < TYT; ++r)
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        const int x = gx + c, y = gy + r, zz = zs - 1;
+        eprev[r][c] = (zz >= 0 && x < P.nx && y < P.ny) ? __ldg(P.eta + ((int64_t)zz * P.ny + y) * P.pitch + x) : 0.f;
+      }
+  }
+
   // ---- warm-up: planes zs-4 .. zs+3 (stages 0..7, first use) -> queue ----
   V q[9][TYT];
 #pragma unroll
@@ -744,6 +768,55 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
           X[r][XC + e] = vget(Y[R + r], e);
         }
       T L[TYT][NV];
+      // fp32: the 25-point sum on packed pairs of x-points (FMUL2/FADD2/FFMA2,
+      // bitwise the scalar chain below element by element, half the issue slots)
+      constexpr bool PK = sizeof(T) == 4 && W25_PACKED;
+      if (PK && MODE != MODE_NULL) {
+        f2_t L2[TYT][2];
+        auto pr = [&](const V& v, int h) -> f2_t {
+          return f2_pack((float)vget(v, 2 * h), (float)vget(v, 2 * h + 1));
+        };
+        // centre and x terms scalar (the x-neighbour pairs of odd m straddle
+        // register pairs: repacking them would cost what packing saves), then
+        // y and z terms on pairs -- the same per-element chain order as below
+#pragma unroll
+        for (int r = 0; r < TYT; ++r) {
+          T Lx[NV];
+#pragma unroll
+          for (int c = 0; c < NV; ++c) {
+            Lx[c] = mul_rn(K.c0, vget(Y[R + r], c));
+#pragma unroll
+            for (int m = 1; m <= R; ++m) Lx[c] = fma_rn(K.cx[m - 1], add_rn(X[r][XC + c + m], X[r][XC + c - m]), Lx[c]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) L2[r][h] = f2_pack((float)Lx[2 * h], (float)Lx[2 * h + 1]);
+        }
+#pragma unroll
+        for (int m = 1; m <= R; ++m)
+#pragma unroll
+          for (int r = 0; r < TYT; ++r)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              L2[r][h] = f2_fma(f2_bcast((float)K.cy[m - 1]), f2_add(pr(Y[R + r + m], h), pr(Y[R + r - m], h)),
+                                L2[r][h]);
+#pragma unroll
+        for (int m = 1; m <= R; ++m)
+#pragma unroll
+          for (int r = 0; r < TYT; ++r)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              L2[r][h] = f2_fma(f2_bcast((float)K.cz[m - 1]),
+                                f2_add(pr(q[(s + 4 + m) % 9][r], h), pr(q[(s + 4 - m + 9) % 9][r], h)), L2[r][h]);
+#pragma unroll
+        for (int r = 0; r < TYT; ++r)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float lo, hi;
+            f2_unpack(L2[r][h], lo, hi);
+            L[r][2 * h] = (T)lo;
+            L[r][2 * h + 1] = (T)hi;
+          }
+      } else {
 #pragma unroll
       for (int r = 0; r < TYT; ++r)
 #pragma unroll
@@ -773,6 +846,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
                              add_rn(vget(q[(s + 4 + m) % 9][r], c), vget(q[(s + 4 - m + 9) % 9][r], c)),
                              L[r][c]);
       }
+      }
 
       // 3. u^{n-1}, vdt2 of plane z
       const int po_ = 9 * j + s;             // plane index in the chunk
@@ -783,6 +857,46 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       for (int r = 0; r < TYT; ++r) {
         upv[r] = ldv(sup + sp * C::P_STAGE + po + r * CW);
         vv[r] = ldv(sv + sp * C::P_STAGE + po + r * CW);
+      }
+      float ecur[ES ? TYT : 1][ES ? NV : 1], ecur_xm[ES ? TYT : 1][ES ? NV : 1], ecur_xp[ES ? TYT : 1][ES ? NV : 1];
+      float ecur_ym[ES ? TYT : 1][ES ? NV : 1], ecur_yp[ES ? TYT : 1][ES ? NV : 1], enext[ES ? TYT : 1][ES ? NV : 1];
+      if (ES) {
+        // my eta box cell: row ly*TYT + r + 1, column NV*lx + 4 (+c); phantom
+        // lanes clamp to the box (their results are masked)
+        const int ec = min(NV * lx, CW - NV) + 4;
+        const float* E0 = se + sp * C::E_STAGE;
+#pragma unroll
+        for (int r = 0; r < TYT; ++r) {
+          const float* row = E0 + (ly * TYT + r + 1) * C::EW + ec;
+#pragma unroll
+          for (int c = 0; c < NV; ++c) {
+            ecur[r][c] = row[c];
+            ecur_xm[r][c] = row[c - 1];
+            ecur_xp[r][c] = row[c + 1];
+            ecur_ym[r][c] = row[c - C::EW];
+            ecur_yp[r][c] = row[c + C::EW];
+          }
+        }
+        // z + 1: the next plane's stage (issued ahead by the producer), or
+        // past the chunk end from global memory (0 outside the domain)
+        if (z + 1 < ze) {
+          const int pn = po_ + 1, spn = pn % C::SPN;
+          mbar_wait(&full_p[spn], (pn / C::SPN) & 1);
+          const float* E1 = se + spn * C::E_STAGE;
+#pragma unroll
+          for (int r = 0; r < TYT; ++r)
+#pragma unroll
+            for (int c = 0; c < NV; ++c) enext[r][c] = E1[(ly * TYT + r + 1) * C::EW + ec + c];
+        } else {
+#pragma unroll
+          for (int r = 0; r < TYT; ++r)
+#pragma unroll
+            for (int c = 0; c < NV; ++c) {
+              const int x = gx + c, y = gy + r;
+              enext[r][c] = (z + 1 < P.nzl && x < P.nx && y < P.ny)
+                                ? __ldg(P.eta + ((int64_t)(z + 1) * P.ny + y) * P.pitch + x) : 0.f;
+            }
+        }
       }
       // all smem reads of plane z done: release its stages to the producer
       __syncwarp();
@@ -808,8 +922,22 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
 #pragma unroll
           for (int r = 0; r < TYT; ++r) {
             T o[NV];
+            if (PK) {
 #pragma unroll
-            for (int c = 0; c < NV; ++c) o[c] = upd_inner(L[r][c], vget(Y[R + r], c), vget(upv[r], c), vget(vv[r], c));
+              for (int h = 0; h < 2; ++h) {
+                float lo, hi;
+                f2_unpack(f2_upd_inner(f2_pack((float)L[r][2 * h], (float)L[r][2 * h + 1]),
+                                       f2_pack((float)vget(Y[R + r], 2 * h), (float)vget(Y[R + r], 2 * h + 1)),
+                                       f2_pack((float)vget(upv[r], 2 * h), (float)vget(upv[r], 2 * h + 1)),
+                                       f2_pack((float)vget(vv[r], 2 * h), (float)vget(vv[r], 2 * h + 1))),
+                          lo, hi);
+                o[2 * h] = (T)lo;
+                o[2 * h + 1] = (T)hi;
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < NV; ++c) o[c] = upd_inner(L[r][c], vget(Y[R + r], c), vget(upv[r], c), vget(vv[r], c));
+            }
             res[r] = vmake<T>(o);
           }
         } else {
@@ -831,15 +959,20 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
           }
         }
       } else if (MODE == MODE_WALL_ETA) {
-        // stored (user-supplied) eta: per-point general path, single-slab plans
+        // stored (user-supplied) eta, staged by TMA in the u_prev/vdt2 ring
+        // (box (CW+8) x (TY+2) per plane): x/y neighbours and the point from
+        // plane z's stage, z+1 from the next stage (loaded ahead), z-1 carried
 #pragma unroll
         for (int r = 0; r < TYT; ++r) {
           T xpa[NV], xma[NV];
 #pragma unroll
           for (int c = 0; c < NV; ++c) { xpa[c] = X[r][XC + c + 1]; xma[c] = X[r][XC + c - 1]; }
-          res[r] = pml_row_eta<T>(vmake<T>(L[r]), Y[R + r], upv[r], vv[r], vmake<T>(xpa), vmake<T>(xma),
-                                  Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], gx, gy + r, z,
-                                  PG, P.eta, P.pitch, P.nzl, P.dt);
+          res[r] = pml_row_eta_s<T>(vmake<T>(L[r]), Y[R + r], upv[r], vv[r], vmake<T>(xpa), vmake<T>(xma),
+                                    Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], gx, gy + r, z,
+                                    PG, ecur[r], ecur_xm[r], ecur_xp[r], ecur_ym[r], ecur_yp[r], eprev[r], enext[r],
+                                    P.dt);
+#pragma unroll
+          for (int c = 0; c < NV; ++c) eprev[r][c] = ecur[r][c];
         }
       } else if (wallw && wkind != 0 && kg > P.w && kg < P.nzg - P.w - 1) {
         // wall, z-interior plane, pure y-wall rows (g = gy) or pure x-wall

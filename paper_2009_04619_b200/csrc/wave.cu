@@ -68,7 +68,7 @@ struct KInfo {
 template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0, typename T = float, int PAIR = 0,
           int CL = 1>
 static KInfo kinfo(const char* name) {
-  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T>;
+  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T, MODE == MODE_WALL_ETA>;
   // tx = width of the u TMA box minus its halo (the half width for split boxes)
   return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR, CL>, C::HW, CW, TY, C::NT, &C::smem_bytes,
                name, CL};
@@ -756,6 +756,11 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   p.kd = P->coefd;
   p.tab = P->tab_d;
   p.eta = P->eta_on ? P->eta_buf : nullptr;
+  if (P->eta_on && (ki == KI_WALLX_E || ki == KI_WALLY_E)) {
+    // the stored eta, staged through the u_prev/vdt2 ring: box (CW + 8) x (TY + 2)
+    const uint64_t pb = P->L.pitch_x * 4;
+    encode3d(&p.tm_eta, P->eta_buf, P->d.nx, P->d.ny, P->d.nz, pb, pb * P->d.ny, CW + 8, TY + 2, false);
+  }
   p.dt = (double)P->dt;
   p.cz = cz;
   p.pf = (is_wall(ki) && P->wall_pf >= 0) ? P->wall_pf : P->pf;
