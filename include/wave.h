@@ -182,6 +182,21 @@ WAVE_API wave_status wave_layout(const wave_desc *desc, wave_layout_info *out);
  * extended domain nx*ny*nz_global.  out must hold 7. */
 WAVE_API wave_status wave_decompose(const wave_desc *desc, wave_region *out);
 
+/* The PML divisors of an fp32 plan, B_d = fp32(1 + eta_d dt) for d = 0..w
+ * (the denominator of the SPEC.md L152 update), and rB_d = RN(1/B_d), the
+ * correctly rounded reciprocal (host arithmetic, exact).  The kernels divide
+ * a numerator n by a table B_d as q0 = RN(n rB), q = RN(q0 + RN(n - q0 B) rB)
+ * (Markstein's FMA correction) when a plan's exhaustive device check has shown
+ * it equal to the IEEE quotient RN(n / B_d) for every fp32 n of the binades
+ * covering the range used (see wave_fastdiv; R9).  Uses desc->dt
+ * (> 0); B and rB (either may be NULL) hold w + 1 floats.  Host memory. */
+WAVE_API wave_status wave_division_table(const wave_desc *desc, float *B, float *rB);
+
+/* 1 if the plan divides by its PML table through the verified Markstein
+ * correction, 0 if by the IEEE division (fp64 plans, WAVE25_FASTDIV=0, or a
+ * failed check), -1 on NULL. */
+WAVE_API int32_t wave_fastdiv(const wave_plan *plan);
+
 /* fp32 constants the plan uses, computed in fp64 and rounded once:
  * c13 = {c_xyz, c_x1..4, c_y1..4, c_z1..4},
  * eta/A/B[w+1] = eta_max (d/w)^2, 1 - eta dt, 1 + eta dt (SPEC.md L152,

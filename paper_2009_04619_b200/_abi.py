@@ -36,6 +36,7 @@ EXPORTS = [
     "wave_step_profiled", "wave_set_peers", "wave_step_peer", "wave_push_halo",
     "wave_plan_bind_aux", "wave_launches", "wave_steps_per_launch", "wave_plan_bind_eta", "wave_set_eta",
     "wave_ipc_export", "wave_ipc_import", "wave_ipc_release", "wave_set_peer_timeout", "wave_peer_check",
+    "wave_division_table", "wave_fastdiv",
 ]
 KERNEL_KINDS = ["interior", "xwalls", "ywalls", "source"]
 
@@ -127,6 +128,8 @@ def lib() -> ctypes.CDLL:
                 "wave_ipc_release": ([P], i32),
                 "wave_set_peer_timeout": ([P, ctypes.c_double], i32),
                 "wave_peer_check": ([P, P], i32),
+                "wave_division_table": ([DP, P, P], i32),
+                "wave_fastdiv": ([P], i32),
             }
             for name, (args, res) in sig.items():
                 fn = getattr(L, name)
@@ -177,6 +180,20 @@ def wave_constants(desc: WaveDesc) -> dict:
     check(lib().wave_constants(ctypes.byref(desc), p(c13), p(eta), p(A), p(B), p(i2h)))
     return {"c_xyz": c13[0], "c_x": c13[1:5], "c_y": c13[5:9], "c_z": c13[9:13],
             "eta": eta, "A": A, "B": B, "inv2h": i2h}
+
+
+def wave_division_table(desc: WaveDesc):
+    """(B[w+1], rB[w+1]): the PML divisors of an fp32 plan and their RN reciprocals."""
+    import numpy as np
+    w = desc.pml_width
+    B, rB = np.zeros(w + 1, np.float32), np.zeros(w + 1, np.float32)
+    check(lib().wave_division_table(ctypes.byref(desc), B.ctypes.data_as(ctypes.c_void_p),
+                                    rB.ctypes.data_as(ctypes.c_void_p)))
+    return B, rB
+
+
+def wave_fastdiv(plan) -> int:
+    return int(lib().wave_fastdiv(plan))
 
 
 def wave_plan_create(desc: WaveDesc) -> ctypes.c_void_p:

@@ -210,6 +210,26 @@ __global__ void k_inc(T* __restrict__ inc, const float* __restrict__ wl, int64_t
     inc[i] = (T)(vs * (double)wl[i]);
 }
 
+// Exhaustive check of the table division (common.cuh div_table, Markstein's
+// reciprocal + FMA correction) against the IEEE division for one plan's B_d:
+// every fp32 significand of n in the binades [1, 2) and [2^-80, 2^-79) (the
+// smallest |n| the fast path takes) for every d (blockIdx.y).  Negative n
+// negates every step exactly (RN is sign-symmetric), and scaling n by 2^k
+// scales q0, the residual and q exactly while they stay normal, so these
+// binades cover every n the fast path accepts.  mism[0] counts differences.
+__global__ void k_divcheck(const float* __restrict__ tab, int T, unsigned* mism) {
+  const float B = tab[2 * T + blockIdx.y], rB = tab[3 * T + blockIdx.y];
+  unsigned bad = 0;
+  for (unsigned m = blockIdx.x * blockDim.x + threadIdx.x; m < (1u << 23); m += gridDim.x * blockDim.x)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const float n = __uint_as_float(((k == 0 ? 127u : 47u) << 23) | m);   // 2^0 and 2^-80 binades
+      const float a = div_table(n, B, rB, true), b = __fdiv_rn(n, B);
+      bad += __float_as_uint(a) != __float_as_uint(b);
+    }
+  if (bad) atomicAdd(mism, bad);
+}
+
 struct Stats {
   unsigned int max_bits;       // max |x| as float bits (finite values only)
   unsigned int min_bits;       // min x as float bits (positive values only)

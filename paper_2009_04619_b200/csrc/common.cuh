@@ -124,6 +124,60 @@ __device__ __forceinline__ f2_t f2_upd_inner(f2_t L, f2_t c, f2_t up, f2_t v) {
   return f2_fma(v, L, f2_sub(f2_add(c, c), up));
 }
 
+// PML division by a TABLE value B with its correctly rounded reciprocal rB =
+// RN(1/B) (R9 / SURVEY A20): q0 = RN(n rB), e = RN(n - q0 B) (exact,
+// FMA), q = RN(q0 + e rB) -- Markstein's correction, equal to RN(n / B) for
+// every n whose result and residual stay normal.  The plan verifies that claim
+// EXHAUSTIVELY for its own B values over every fp32 significand at setup
+// (k_divcheck; fast = false if any differs), and |n| < 2^-80 (residual could
+// be subnormal) takes the IEEE division.  Branch-free on the common path: no
+// MUFU, no slow-path call, 3 dependent operations instead of ~10.
+template <typename T>
+__device__ __forceinline__ T div_table(T n, T B, T rB, bool fast) {
+  if (!fast) return div_rn(n, B);
+  if (fabs(n) < T(0x1p-80)) return n == T(0) ? n : div_rn(n, B);
+  const T q0 = mul_rn(n, rB);
+  return fma_rn(fma_rn(-q0, B, n), rB, q0);
+}
+
+// div_table on the NV points of a lane, straight-line: all fast quotients
+// first (independent chains interleave), then one rarely taken fix-up for
+// tiny or zero numerators.  Bitwise div_table per element.
+template <typename T, int N>
+__device__ __forceinline__ void div_table_row(const T* n, const T* B, const T* rB, bool fast, T* q) {
+  if (!fast) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) q[c] = n[c] == T(0) ? n[c] : div_rn(n[c], B[c]);
+    return;
+  }
+  bool tiny = false;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    tiny |= fabs(n[c]) < T(0x1p-80);
+    const T q0 = mul_rn(n[c], rB[c]);
+    q[c] = fma_rn(fma_rn(-q0, B[c], n[c]), rB[c], q0);
+  }
+  if (tiny) {
+#pragma unroll
+    for (int c = 0; c < N; ++c)
+      if (fabs(n[c]) < T(0x1p-80)) q[c] = n[c] == T(0) ? n[c] : div_rn(n[c], B[c]);
+  }
+}
+
+// numerator of the PML update: (2u - A u_prev) + vdt2 (L + g)
+template <typename T>
+__device__ __forceinline__ T pml_num(T L, T g, T c, T up, T v, T A) {
+  return fma_rn(v, add_rn(L, g), fma_rn(-A, up, mul_rn(T(2), c)));
+}
+
+// upd_pml with a table B (and its reciprocal): bitwise upd_pml
+template <typename T>
+__device__ __forceinline__ T upd_pml_t(T L, T g, T c, T up, T v, T A, T B, T rB, bool fast) {
+  const T t = fma_rn(-A, up, mul_rn(T(2), c));
+  const T num = fma_rn(v, add_rn(L, g), t);
+  return div_table(num, B, rB, fast);
+}
+
 // 16-byte vector of the precision: 4 floats or 2 doubles per lane
 template <typename T> struct VecT;
 template <> struct VecT<float> { using V = float4; static constexpr int N = 4; };

@@ -75,7 +75,9 @@ struct StreamParams {
   Region reg[MAX_REGIONS];
   Coef k;                       // fp32 plans
   CoefT<double> kd;             // fp64 plans
-  const void* tab;              // [3][w+2] (T): eta_d, A_d, B_d (d = 0..w), eta_{w+1} = 0
+  const void* tab;              // [4][w+2] (T): eta_d, A_d, B_d, RN(1/B_d) (d = 0..w), eta_{w+1} = 0
+  int fastdiv;                  // divide by table B values as Markstein n*rB + FMA correction (verified
+                                // bitwise == RN(n/B) for this plan's B at setup; common.cuh div_table)
   // tensor maps in global memory (one per buffer, never rewritten) used instead
   // of the __grid_constant__ copies when non-null (WAVE25_GMAPS)
   const CUtensorMap* gu;
@@ -169,13 +171,13 @@ struct StreamCfg {
   // stages), so more of those two streams is in flight per SM
   static constexpr int fits_(int n) {
     return (SU * U_STAGE + 2 * n * P_STAGE) * (int)sizeof(T) + n * E_STAGE * 4 + 2 * (SU + n) * 8 +
-               3 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
+               4 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
   }
   static constexpr int SPN = (W25_SP_MAX >= 5 && fits_(5)) ? 5 : (W25_SP_MAX >= 4 && fits_(4)) ? 4 : 3;
   static constexpr int E_OFF = (SU * U_STAGE + 2 * SPN * P_STAGE) * (int)sizeof(T);    // bytes (eta ring)
   static constexpr int BAR_OFF = E_OFF + SPN * E_STAGE * 4;                             // bytes
   static constexpr int TAB_OFF = BAR_OFF + 2 * (SU + SPN) * 8;
-  static size_t smem_bytes(int w) { return TAB_OFF + 3 * (w + 2) * sizeof(T); }
+  static size_t smem_bytes(int w) { return TAB_OFF + 4 * (w + 2) * sizeof(T); }
   static_assert(CW % 4 == 0 && CW <= TX && TX % 4 == 0, "tile widths");
   static_assert(32 % LXW == 0 && (TY / TYT) % LYW == 0 && TY % TYT == 0, "warp tiling");
   static_assert((U_HALF * sizeof(T)) % 128 == 0 && (P_STAGE * sizeof(T)) % 128 == 0 && (E_STAGE * 4) % 128 == 0,
@@ -190,7 +192,7 @@ struct PmlGeoT { int nx, ny, nzg, w, TN; T i2hx, i2hy, i2hz; };
 
 // Plane-uniform constants of a z-PML cap plane seen from the inner xy footprint.
 template <typename T>
-struct CapCT { T ex, ezp, ezm, A, B; };
+struct CapCT { T ex, ezp, ezm, A, B, rB; };
 
 // PML update of one vector row inside a z cap (inner x,y => eta(x+-1) =
 // eta(y+-1) = eta_dz); same arithmetic as the naive kernel's PML branch.
@@ -200,7 +202,7 @@ __device__ __noinline__ typename VecT<T>::V cap_update(typename VecT<T>::V L, ty
                                                        typename VecT<T>::V xp, typename VecT<T>::V xm,
                                                        typename VecT<T>::V yp, typename VecT<T>::V ym,
                                                        typename VecT<T>::V zp, typename VecT<T>::V zm,
-                                                       CapCT<T> cc, T i2hx, T i2hy, T i2hz) {
+                                                       CapCT<T> cc, T i2hx, T i2hy, T i2hz, bool fast = false) {
   constexpr int NV = VecT<T>::N;
   T res[NV];
 #pragma unroll
@@ -208,7 +210,7 @@ __device__ __noinline__ typename VecT<T>::V cap_update(typename VecT<T>::V L, ty
     const T g = add_rn(add_rn(gterm(cc.ex, cc.ex, vget(xp, c), vget(xm, c), i2hx),
                               gterm(cc.ex, cc.ex, vget(yp, c), vget(ym, c), i2hy)),
                        gterm(cc.ezp, cc.ezm, vget(zp, c), vget(zm, c), i2hz));
-    res[c] = upd_pml(vget(L, c), g, vget(C, c), vget(up, c), vget(v, c), cc.A, cc.B);
+    res[c] = upd_pml_t(vget(L, c), g, vget(C, c), vget(up, c), vget(v, c), cc.A, cc.B, cc.rB, fast);
   }
   return vmake<T>(res);
 }
@@ -224,7 +226,7 @@ __device__ __noinline__ typename VecT<T>::V pml_row_call(typename VecT<T>::V L, 
                                                          typename VecT<T>::V xp, typename VecT<T>::V xm,
                                                          typename VecT<T>::V yp, typename VecT<T>::V ym,
                                                          typename VecT<T>::V zp, typename VecT<T>::V zm, int gx,
-                                                         int gy, int kg, PmlGeoT<T> G, const T* stab) {
+                                                         int gy, int kg, PmlGeoT<T> G, const T* stab, bool fast) {
   constexpr int NV = VecT<T>::N;
   const int dy = dist1(gy, G.ny, G.w), dyp = dist1(gy + 1, G.ny, G.w), dym = dist1(gy - 1, G.ny, G.w);
   const int dz = dist1(kg, G.nzg, G.w), dzp = dist1(kg + 1, G.nzg, G.w), dzm = dist1(kg - 1, G.nzg, G.w);
@@ -248,7 +250,7 @@ __device__ __noinline__ typename VecT<T>::V pml_row_call(typename VecT<T>::V L, 
       const T g = add_rn(add_rn(gterm(exp_, exm, vget(xp, c), vget(xm, c), G.i2hx),
                                 gterm(eyp, eym, vget(yp, c), vget(ym, c), G.i2hy)),
                          gterm(ezp, ezm, vget(zp, c), vget(zm, c), G.i2hz));
-      res[c] = upd_pml(Lc, g, uc, upc, vc, stab[G.TN + d], stab[2 * G.TN + d]);
+      res[c] = upd_pml_t(Lc, g, uc, upc, vc, stab[G.TN + d], stab[2 * G.TN + d], stab[3 * G.TN + d], fast);
     }
   }
   return vmake<T>(res);
@@ -413,7 +415,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     for (int s = 0; s < C::SPN; ++s) { mbar_init(&full_p[s], 1); mbar_init(&empty_p[s], C::NWC); }
     fence_mbar_init();
   }
-  for (int i = tid; i < 3 * TABN; i += C::NT) stab[i] = static_cast<const T*>(P.tab)[i];
+  for (int i = tid; i < 4 * TABN; i += C::NT) stab[i] = static_cast<const T*>(P.tab)[i];
   if (PAIR && tid < 16) s_arr[tid] = 0;
   __syncthreads();
   if (CL > 1) cluster_sync_all();            // peers' barriers initialised before any multicast / remote arrive
@@ -628,8 +630,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   // general path's call, and the LDL latency stalled the wall kernels (§5).
   int wkind = 0;                             // 1: y-wall rows, 2: x-wall columns, 0: general
   constexpr bool WT = MODE == MODE_WALL || MODE == MODE_FUSED;
-  __shared__ __align__(16) T s_wc[WT ? 3 * CW : 1];   // per column: cg_x, A, B
-  __shared__ __align__(16) T s_wr[WT ? 3 * TY : 1];   // per row: cg_y, A, B
+  __shared__ __align__(16) T s_wc[WT ? 4 * CW : 1];   // per column: cg_x, A, B, RN(1/B)
+  __shared__ __align__(16) T s_wr[WT ? 4 * TY : 1];   // per row: cg_y, A, B, RN(1/B)
   const int wci = min(NV * lx, CW - NV);     // my first table column (phantom lanes clamp)
   // fused mode: warps touching the x/y PML take the same specialised paths
   const bool wallw = MODE == MODE_WALL || MODE == MODE_WALL_ETA || (MODE == MODE_FUSED && warp_xy_pml);
@@ -659,6 +661,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
                              PG.i2hy);
         s_wr[TY + ly * TYT + r] = stab[TABN + dy];
         s_wr[2 * TY + ly * TYT + r] = stab[2 * TABN + dy];
+        s_wr[3 * TY + ly * TYT + r] = stab[3 * TABN + dy];
       }
     }
     if (ly == 0 && NV * lx < CW) {           // one writer per tile column
@@ -671,6 +674,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
                              PG.i2hx);
         s_wc[CW + NV * lx + c] = stab[TABN + dx];
         s_wc[2 * CW + NV * lx + c] = stab[2 * TABN + dx];
+        s_wc[3 * CW + NV * lx + c] = stab[3 * TABN + dx];
       }
     }
     // consumer warps only (the producer warps have left): named barrier 1
@@ -948,6 +952,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
           cc.ezm = stab[dist1(kg - 1, P.nzg, P.w)];
           cc.A = stab[TABN + dz];
           cc.B = stab[2 * TABN + dz];
+          cc.rB = stab[3 * TABN + dz];
 #pragma unroll
           for (int r = 0; r < TYT; ++r) {
             T xpa[NV], xma[NV];
@@ -955,7 +960,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
             for (int c = 0; c < NV; ++c) { xpa[c] = X[r][XC + c + 1]; xma[c] = X[r][XC + c - 1]; }
             res[r] = cap_update<T>(vmake<T>(L[r]), Y[R + r], upv[r], vv[r], vmake<T>(xpa), vmake<T>(xma),
                                    Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], cc, K.i2h[0],
-                                   K.i2h[1], K.i2h[2]);
+                                   K.i2h[1], K.i2h[2], P.fastdiv != 0);
           }
         }
       } else if (MODE == MODE_WALL_ETA) {
@@ -980,22 +985,29 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
 #pragma unroll
         for (int r = 0; r < TYT; ++r) {
           T o[NV];
+          T num[NV], Bd[NV], rBd[NV];
           if (wkind == 1) {
             const int ri = ly * TYT + r;
-            const T cg = s_wr[ri], Aw = s_wr[TY + ri], Bw = s_wr[2 * TY + ri];
+            const T cg = s_wr[ri], Aw = s_wr[TY + ri], Bw = s_wr[2 * TY + ri], rBw = s_wr[3 * TY + ri];
 #pragma unroll
             for (int c = 0; c < NV; ++c) {
               const T gya = mul_rn(cg, mul_rn(sub_rn(vget(Y[R + r + 1], c), vget(Y[R + r - 1], c)), K.i2h[1]));
-              o[c] = upd_pml(L[r][c], gya, X[r][XC + c], vget(upv[r], c), vget(vv[r], c), Aw, Bw);
+              num[c] = pml_num(L[r][c], gya, X[r][XC + c], vget(upv[r], c), vget(vv[r], c), Aw);
+              Bd[c] = Bw;
+              rBd[c] = rBw;
             }
           } else {
             const V cgv = ldv(s_wc + wci), Av = ldv(s_wc + CW + wci), Bv = ldv(s_wc + 2 * CW + wci);
+            const V rBv = ldv(s_wc + 3 * CW + wci);
 #pragma unroll
             for (int c = 0; c < NV; ++c) {
               const T gxa = mul_rn(vget(cgv, c), mul_rn(sub_rn(X[r][XC + c + 1], X[r][XC + c - 1]), K.i2h[0]));
-              o[c] = upd_pml(L[r][c], gxa, X[r][XC + c], vget(upv[r], c), vget(vv[r], c), vget(Av, c), vget(Bv, c));
+              num[c] = pml_num(L[r][c], gxa, X[r][XC + c], vget(upv[r], c), vget(vv[r], c), vget(Av, c));
+              Bd[c] = vget(Bv, c);
+              rBd[c] = vget(rBv, c);
             }
           }
+          div_table_row<T, NV>(num, Bd, rBd, P.fastdiv != 0, o);
           res[r] = vmake<T>(o);
         }
       } else {
@@ -1008,7 +1020,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
           for (int c = 0; c < NV; ++c) { xpa[c] = X[r][XC + c + 1]; xma[c] = X[r][XC + c - 1]; }
           res[r] = pml_row_call<T>(vmake<T>(L[r]), Y[R + r], upv[r], vv[r], vmake<T>(xpa), vmake<T>(xma),
                                    Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], gx, gy + r,
-                                   kg, PG, stab);
+                                   kg, PG, stab, P.fastdiv != 0);
         }
       }
       if (PAIR && src_r >= 0 && z == P.src_k) {

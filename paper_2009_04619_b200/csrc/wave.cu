@@ -11,6 +11,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -21,7 +23,6 @@
 #include "stream.cuh"
 #include "tb2.cuh"
 #include "paper_shapes.cuh"
-#include <map>
 
 using namespace w25;
 
@@ -295,6 +296,8 @@ struct wave_plan {
   int wall_cz = 0;                   // WAVE25_WALL_CZ: wall chunk length (0 = auto)
   int xwall_extra = 0;               // WAVE25_XWALL_EXTRA: inner columns computed by the x-wall kernel
   bool xinter = true;                // WAVE25_XINTER=0: x-wall launch region-major instead of left/right interleaved
+  bool fastdiv_on = true;            // WAVE25_FASTDIV=0: IEEE division in the PML updates (A/B)
+  bool fastdiv = false;              // table division verified bitwise for this plan (check_fastdiv)
   bool walls_last = false;           // WAVE25_WALLS_LAST: enqueue the wall kernels after the interior
   int mix = 0;                       // WAVE25_MIX=1/2: interior + x walls as one grid (k_mix, §5i; measured slower)
   bool mix_ok = false;               // geometry / kernel choice supports k_mix (set by build_launches)
@@ -463,7 +466,7 @@ static void make_constants64(const wave_desc& d, float dt, CoefT<double>* k, std
   }
   for (int a = 0; a < 3; ++a) k->i2h[a] = 1.0 / (2.0 * (a == 0 ? d.hx : a == 1 ? d.hy : d.hz));
   const int w = d.pml_width, T = w + 2;
-  tab->assign(3 * T, 0.0);
+  tab->assign(4 * T, 0.0);
   for (int dd = 0; dd <= w; ++dd) {
     const double r = w > 0 ? (double)dd / (double)w : 0.0;
     const double eta = d.eta_max * r * r;
@@ -474,6 +477,22 @@ static void make_constants64(const wave_desc& d, float dt, CoefT<double>* k, std
   (*tab)[w + 1] = 0.0;
   (*tab)[T + w + 1] = 1.0;
   (*tab)[2 * T + w + 1] = 1.0;
+  for (int i = 0; i < T; ++i) (*tab)[3 * T + i] = 1.0 / (*tab)[2 * T + i];   // unused (fp64 divides)
+}
+
+// RN(1/B) in fp32 exactly: the candidate from fp64 and its two neighbours,
+// the one with the smallest |1 - r B| (exact in fp64: r B has 48 bits and
+// lies within 2^-23 of 1).  1/B is never an fp32 midpoint (B > 1 is not a
+// power of 2), so the minimum is unique.
+static float recip_rn(float B) {
+  const float c = (float)(1.0 / (double)B);
+  float best = c;
+  double be = 2.0;
+  for (float r : {std::nextafter(c, 0.f), c, std::nextafter(c, 2.f)}) {
+    const double e = std::fabs(1.0 - (double)r * (double)B);
+    if (e < be) { be = e; best = r; }
+  }
+  return best;
 }
 
 // fp64 -> fp32 once (R8)
@@ -489,7 +508,7 @@ static void make_constants(const wave_desc& d, float dt, Coef* k, std::vector<fl
   k->i2h[1] = (float)(1.0 / (2.0 * d.hy));
   k->i2h[2] = (float)(1.0 / (2.0 * d.hz));
   const int w = d.pml_width, T = w + 2;
-  tab->assign(3 * T, 0.f);
+  tab->assign(4 * T, 0.f);
   for (int dd = 0; dd <= w; ++dd) {
     const double r = w > 0 ? (double)dd / (double)w : 0.0;
     const double eta = d.eta_max * r * r;                 // eta_max (d/w)^2, R2
@@ -500,6 +519,7 @@ static void make_constants(const wave_desc& d, float dt, Coef* k, std::vector<fl
   (*tab)[w + 1] = 0.f;                                    // outside the domain (R4)
   (*tab)[T + w + 1] = 1.f;
   (*tab)[2 * T + w + 1] = 1.f;
+  for (int i = 0; i < T; ++i) (*tab)[3 * T + i] = recip_rn((*tab)[2 * T + i]);   // RN(1/B_d), common.cuh div_table
 }
 
 // ---------------------------------------------------------------------------
@@ -755,6 +775,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   p.k = P->coef;
   p.kd = P->coefd;
   p.tab = P->tab_d;
+  p.fastdiv = P->fastdiv ? 1 : 0;
   p.eta = P->eta_on ? P->eta_buf : nullptr;
   if (P->eta_on && (ki == KI_WALLX_E || ki == KI_WALLY_E)) {
     // the stored eta, staged through the u_prev/vdt2 ring: box (CW + 8) x (TY + 2)
@@ -1330,6 +1351,23 @@ wave_status wave_constants(const wave_desc* desc, float* c13, float* eta, float*
   return WAVE_OK;
 }
 
+wave_status wave_division_table(const wave_desc* desc, float* B, float* rB) {
+  if (!desc) return fail(WAVE_ERR_CONFIG, "desc is NULL");
+  CKST(validate(desc));
+  if (!(desc->dt > 0.f)) return fail(WAVE_ERR_CONFIG, "wave_division_table needs desc->dt > 0");
+  Coef k;
+  std::vector<float> tab;
+  make_constants(*desc, desc->dt, &k, &tab);
+  const int w = desc->pml_width, T = w + 2;
+  for (int d = 0; d <= w; ++d) {
+    if (B) B[d] = tab[2 * T + d];
+    if (rB) rB[d] = tab[3 * T + d];
+  }
+  return WAVE_OK;
+}
+
+int32_t wave_fastdiv(const wave_plan* P) { return P ? (P->fastdiv ? 1 : 0) : -1; }
+
 wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   CKST(validate(desc));
   if (!out) return fail(WAVE_ERR_CONFIG, "out is NULL");
@@ -1376,6 +1414,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_SIDE2")) P->side2_on = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
   if (const char* e = getenv("WAVE25_XINTER")) P->xinter = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_FASTDIV")) P->fastdiv_on = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_PEER_TIMEOUT_S")) P->peer_timeout_s = std::max(1e-3, atof(e));
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
   if (const char* e = getenv("WAVE25_WALLS_LAST")) P->walls_last = atoi(e) != 0;
@@ -1399,7 +1438,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
     cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>((size_t)P->l2_persist_mb << 20, (size_t)mx));
   }
   const int T = P->d.pml_width + 2;
-  if ((e = cudaMalloc(&P->tab_d, 3 * T * P->esz)) != cudaSuccess ||
+  if ((e = cudaMalloc(&P->tab_d, 4 * T * P->esz)) != cudaSuccess ||
       (e = cudaMalloc(&P->dstep, sizeof(unsigned long long))) != cudaSuccess ||
       (e = cudaMalloc(&P->stats_d, sizeof(Stats))) != cudaSuccess)
     return bail(fail(WAVE_ERR_ALLOC, "cudaMalloc: %s", cudaGetErrorString(e)));
@@ -1474,6 +1513,33 @@ void wave_plan_destroy(wave_plan* P) {
   delete P;
 }
 
+// Is the table division (div_table) bitwise the IEEE division for every B_d of
+// this fp32 table?  Exhaustive device check (k_divcheck), cached per table.
+static wave_status check_fastdiv(wave_plan* P, cudaStream_t s, bool* ok) {
+  static std::mutex mu;
+  static std::map<std::vector<float>, bool> cache;
+  const int T = P->d.pml_width + 2;
+  std::vector<float> key(P->tab_h.begin() + 2 * T, P->tab_h.begin() + 4 * T);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) { *ok = it->second; return WAVE_OK; }
+  }
+  unsigned* d = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(unsigned), s));
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned), s));
+  k_divcheck<<<dim3(4 * 148, T), 256, 0, s>>>(static_cast<const float*>(P->tab_d), T, d);
+  CK(cudaGetLastError());
+  unsigned h = 1;
+  CK(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
+  CK(cudaFreeAsync(d, s));
+  CK(cudaStreamSynchronize(s));
+  *ok = h == 0;
+  std::lock_guard<std::mutex> g(mu);
+  cache[key] = *ok;
+  return WAVE_OK;
+}
+
 static wave_status refresh_tables(wave_plan* P, cudaStream_t s) {
   make_constants(P->d, P->dt, &P->coef, &P->tab_h);
   make_constants64(P->d, P->dt, &P->coefd, &P->tab_hd);
@@ -1482,6 +1548,8 @@ static wave_status refresh_tables(wave_plan* P, cudaStream_t s) {
   else
     CK(cudaMemcpyAsync(P->tab_d, P->tab_h.data(), P->tab_h.size() * sizeof(float), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));   // tab_h is pageable host memory
+  P->fastdiv = false;
+  if (P->prec == 0 && P->fastdiv_on) CKST(check_fastdiv(P, s, &P->fastdiv));
   CKST(build_launches(P));
   drop_graphs(P);
   return WAVE_OK;

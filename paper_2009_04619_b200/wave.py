@@ -240,6 +240,11 @@ class WavePlan:
         return _abi.wave_launches(self._plan, nsteps)
 
     @property
+    def fastdiv(self) -> bool:
+        """True when the PML divisions use the verified table reciprocal (wave_fastdiv)."""
+        return _abi.wave_fastdiv(self._plan) == 1
+
+    @property
     def steps_per_launch(self) -> int:
         """2 when step() runs two-step temporal blocking, else 1."""
         return _abi.wave_steps_per_launch(self._plan)

@@ -401,6 +401,7 @@ for name in ("RAGGED", "C1"):
     {"WAVE25_INNER_TILE": "128x8x1"}, {"WAVE25_INNER_TILE": "248x8x1"}, {"WAVE25_INNER_TILE": "224x8x1"},
     {"WAVE25_INNER_TILE": "248x8x2"}, {"WAVE25_INNER_TILE": "256x8x1r"},
     {"WAVE25_INNER_TILE": "248x8x1rc2"}, {"WAVE25_INNER_TILE": "248x8x1rc4"},
+    {"WAVE25_FASTDIV": "0"}, {"WAVE25_NO_ORIGIN": "1"}, {"WAVE25_XINTER": "0"},
     {"WAVE25_FUSED": "1", "WAVE25_FUSED_TILE": "fused128x8x1"},
     {"WAVE25_ABLATION": "gmem_32x4x1"}, {"WAVE25_ABLATION": "gmem_8x8x8"}, {"WAVE25_ABLATION": "smem_u"},
     {"WAVE25_ABLATION": "st_smem_32x16"}, {"WAVE25_ABLATION": "st_reg_shft_32x16"},
@@ -413,6 +414,8 @@ for name in ("RAGGED", "C1"):
     {"WAVE25_ORDER": "-3"}, {"WAVE25_ORDER": "2"}, {"WAVE25_MIX": "1"}, {"WAVE25_MIX": "2"}, {"WAVE25_SIDE2": "0"}, {"WAVE25_WALL_CZ": "114"},
 ])
 def test_kernel_variants_bitwise(env):
+    # (WAVE25_FASTDIV=0: IEEE divisions instead of the verified table
+    # reciprocal -- bitwise the same by the setup check, R9)
     # every tile / scheduling variant used in the DESIGN.md ablations computes
     # the same values as the default configuration, bitwise
     import os
@@ -698,3 +701,19 @@ def test_mirror_symmetry_bitwise_full_size(precision):
     assert np.isfinite(u).all() and np.abs(u).max() > 0
     for ax in range(3):
         assert np.array_equal(u, np.flip(u, axis=ax)), ax
+
+
+@pytest.mark.parametrize("name", ["C1", "RAGGED", "SPEC48"])
+def test_table_division_verified_and_used(name):
+    # the plan's exhaustive device check (k_divcheck over every fp32
+    # significand, R9) accepted the Markstein table division for the
+    # fp32 configurations, and fp64 plans keep the IEEE division
+    s = synth.scenario(name)
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    p.set_velocity(synth.velocity(s))
+    assert p.fastdiv
+    p.close()
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, precision="fp64")
+    p.set_velocity(synth.velocity(s))
+    assert not p.fastdiv
+    p.close()
