@@ -204,14 +204,17 @@ __device__ __noinline__ typename VecT<T>::V cap_update(typename VecT<T>::V L, ty
                                                        typename VecT<T>::V zp, typename VecT<T>::V zm,
                                                        CapCT<T> cc, T i2hx, T i2hy, T i2hz, bool fast = false) {
   constexpr int NV = VecT<T>::N;
-  T res[NV];
+  T num[NV], Bd[NV], rBd[NV], res[NV];
 #pragma unroll
   for (int c = 0; c < NV; ++c) {
     const T g = add_rn(add_rn(gterm(cc.ex, cc.ex, vget(xp, c), vget(xm, c), i2hx),
                               gterm(cc.ex, cc.ex, vget(yp, c), vget(ym, c), i2hy)),
                        gterm(cc.ezp, cc.ezm, vget(zp, c), vget(zm, c), i2hz));
-    res[c] = upd_pml_t(vget(L, c), g, vget(C, c), vget(up, c), vget(v, c), cc.A, cc.B, cc.rB, fast);
+    num[c] = pml_num(vget(L, c), g, vget(C, c), vget(up, c), vget(v, c), cc.A);
+    Bd[c] = cc.B;
+    rBd[c] = cc.rB;
   }
+  div_table_row<T, NV>(num, Bd, rBd, fast, res);
   return vmake<T>(res);
 }
 
