@@ -501,7 +501,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     };
     // p plane p (p >= zs) lives in p stage (p - zs) % 3, use (p - zs) / 3
     auto issue_p = [&](int p, int st) {
-      mbar_arrive_expect_tx(&full_p[st], 2 * C::P_STAGE * sizeof(T) + C::E_STAGE * 4);
+      // (the eta box delivers EW x (TY+2) floats; E_STAGE is that rounded up for alignment)
+      mbar_arrive_expect_tx(&full_p[st], 2 * C::P_STAGE * sizeof(T) + (MODE == MODE_WALL_ETA ? C::EW * (TY + 2) * 4 : 0));
       tma_load_3d(sup + st * C::P_STAGE, mup, &full_p[st], cx0, ty0, p + R, pol_s);
       tma_load_3d(sv + st * C::P_STAGE, mv, &full_p[st], cx0, ty0, p, pol_s);
       if (MODE == MODE_WALL_ETA) tma_load_3d(se + st * C::E_STAGE, &P.tm_eta, &full_p[st], cx0 - 4, ty0 - 1, p, pol_s);
