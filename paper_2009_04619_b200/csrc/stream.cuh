@@ -177,7 +177,13 @@ struct StreamCfg {
   static constexpr int E_OFF = (SU * U_STAGE + 2 * SPN * P_STAGE) * (int)sizeof(T);    // bytes (eta ring)
   static constexpr int BAR_OFF = E_OFF + SPN * E_STAGE * 4;                             // bytes
   static constexpr int TAB_OFF = BAR_OFF + 2 * (SU + SPN) * 8;
-  static size_t smem_bytes(int w) { return TAB_OFF + 4 * (w + 2) * sizeof(T); }
+  // u boxes whose rows are exactly one 128-B line (the fp32 x walls, 24 + 8
+  // floats) are loaded with the TMA 128-B swizzle: a float4 column read across
+  // the 8 rows of a warp would otherwise hit the same 16 banks (2 wavefronts
+  // per 128 B); swizzled stages need 1024-B alignment
+  static constexpr bool SWZ = NH == 1 && SW * (int)sizeof(T) == 128 && (U_HALF * (int)sizeof(T)) % 1024 == 0;
+  static constexpr int ALIGN_PAD = SWZ ? 1024 : 0;
+  static size_t smem_bytes(int w) { return ALIGN_PAD + TAB_OFF + 4 * (w + 2) * sizeof(T); }
   static_assert(CW % 4 == 0 && CW <= TX && TX % 4 == 0, "tile widths");
   static_assert(32 % LXW == 0 && (TY / TYT) % LYW == 0 && TY % TYT == 0, "warp tiling");
   static_assert((U_HALF * sizeof(T)) % 128 == 0 && (P_STAGE * sizeof(T)) % 128 == 0 && (E_STAGE * 4) % 128 == 0,
@@ -320,7 +326,9 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   const int crank = CL > 1 ? (int)cluster_ctarank() : 0;
   constexpr int KX = (R + NV - 1) / NV;           // x-neighbour vectors on each side
   constexpr int XC = KX * NV;                     // index of the first centre point in X[]
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_dyn[];
+  // (swizzled u stages: the layout starts at the next 1024-B boundary)
+  unsigned char* smem_raw = smem_dyn + (C::SWZ ? ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u) : 0u);
   T* su = reinterpret_cast<T*>(smem_raw);
   T* sup = su + SU * C::U_STAGE;
   T* sv = sup + C::SPN * C::P_STAGE;
@@ -593,6 +601,19 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     return colo + (CL > 1 ? ((lyf + jj) & (4 * R - 1)) : (lyf + jj)) * C::SW;
   };
   const int uo = yo(R);                     // my first own row
+  // swizzled stages (C::SWZ): element offset of the float4 chunk `ch` of box row `rr`
+  const int kc = (cxo + NV * lx + R) / NV;  // my centre chunk
+  auto uz = [&](int rr, int ch) -> int { return rr * C::SW + ((ch ^ (rr & 7)) * NV); };
+  // my centre-chunk column of window rows ly*TYT + j, j = 0..7 (row j+8 repeats
+  // row j), packed 3 bits per row in one register (9 hoisted offsets spilled)
+  unsigned zsw = 0;
+  if (C::SWZ) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) zsw |= (unsigned)((kc ^ ((ly * TYT + j) & 7)) & 7) << (3 * j);
+  }
+  auto uzc = [&](int jj) -> int {             // u-stage offset of window row ly*TYT + jj, my centre chunk
+    return (ly * TYT + jj) * C::SW + (int)((zsw >> (3 * (jj & 7))) & 7u) * NV;
+  };
   const int po = (ly * TYT) * CW + NV * lx;
 
   // ---- per-thread geometry: store mask, PML coefficients -----------------
@@ -721,7 +742,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   for (int s = 0; s < 8; ++s) {
     mbar_wait(&full_u[s], 0);
 #pragma unroll
-    for (int r = 0; r < TYT; ++r) q[s][r] = ldv(su + s * C::U_STAGE + uo + r * C::SW);
+    for (int r = 0; r < TYT; ++r)
+      q[s][r] = ldv(su + s * C::U_STAGE + (C::SWZ ? uzc(R + r) : uo + r * C::SW));
   }
   __syncwarp();
   if (lane == 0) {                           // planes zs-4..zs-1 are not needed again
@@ -744,15 +766,20 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       // 1. leading plane z+4 -> queue
       mbar_wait(&full_u[sl], (j + (s >= 1 ? 1 : 0)) & 1);
 #pragma unroll
-      for (int r = 0; r < TYT; ++r) q[sl][r] = ldv(su + sl * C::U_STAGE + uo + r * C::SW);
+      for (int r = 0; r < TYT; ++r)
+        q[sl][r] = ldv(su + sl * C::U_STAGE + (C::SWZ ? uzc(R + r) : uo + r * C::SW));
 
       // 2. Laplacian of all NV*TYT points (interleaved chains)
       const T* S = su + sc * C::U_STAGE + uo;
+      // swizzled stages: re-derive the row offsets from the packed register
+      // every plane (hoisted, the 9 offsets would spill)
+      int kcv = kc;
+      if (C::SWZ) asm volatile("" : "+r"(zsw), "+r"(kcv));
       V Y[TYT + 2 * R];                      // rows -4 .. TYT+3 at my vector
 #pragma unroll
       for (int jj = 0; jj < TYT + 2 * R; ++jj) {
         if (jj >= R && jj < R + TYT) Y[jj] = q[sc][jj - R];
-        else Y[jj] = ldv(su + sc * C::U_STAGE + yo(jj));
+        else Y[jj] = ldv(su + sc * C::U_STAGE + (C::SWZ ? uzc(jj) : yo(jj)));
       }
       // x neighbours: KX vectors on each side of the centre vector
       V XL[TYT][KX], XR[TYT][KX];
@@ -760,8 +787,16 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       for (int r = 0; r < TYT; ++r)
 #pragma unroll
         for (int k = 0; k < KX; ++k) {
-          XL[r][k] = ldv(S + r * C::SW - (KX - k) * NV);
-          XR[r][k] = ldv(S + r * C::SW + (k + 1) * NV);
+          if (C::SWZ) {
+            // chunks kc -+ 1 of my own row: the centre chunk's swizzled index xor 1 ... via the packed field
+            const int rr = ly * TYT + R + r;
+            const int cc = (int)((zsw >> (3 * ((R + r) & 7))) & 7u);        // kc ^ (rr & 7)
+            XL[r][k] = ldv(su + sc * C::U_STAGE + rr * C::SW + ((cc ^ (kcv ^ (kcv - (KX - k)))) * NV));
+            XR[r][k] = ldv(su + sc * C::U_STAGE + rr * C::SW + ((cc ^ (kcv ^ (kcv + k + 1))) * NV));
+          } else {
+            XL[r][k] = ldv(S + r * C::SW - (KX - k) * NV);
+            XR[r][k] = ldv(S + r * C::SW + (k + 1) * NV);
+          }
         }
       T X[TYT][(2 * KX + 1) * NV];           // x-4.. of my points, centre at XC
 #pragma unroll
@@ -778,7 +813,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       T L[TYT][NV];
       // fp32: the 25-point sum on packed pairs of x-points (FMUL2/FADD2/FFMA2,
       // bitwise the scalar chain below element by element, half the issue slots)
-      constexpr bool PK = sizeof(T) == 4 && W25_PACKED;
+      constexpr bool PK = sizeof(T) == 4 && W25_PACKED && MODE == MODE_INNER;   // (walls: scalar, no spills)
       if (PK && MODE != MODE_NULL) {
         f2_t L2[TYT][2];
         auto pr = [&](const V& v, int h) -> f2_t {

@@ -64,6 +64,7 @@ struct KInfo {
   size_t (*smem)(int w);
   const char* name;
   int cl = 1;              // thread-block cluster size (y-stacked tiles, multicast u halves)
+  bool swz = false;        // u boxes loaded with the TMA 128-B swizzle (StreamCfg::SWZ)
 };
 
 template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0, typename T = float, int PAIR = 0,
@@ -72,7 +73,7 @@ static KInfo kinfo(const char* name) {
   using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T, MODE == MODE_WALL_ETA>;
   // tx = width of the u TMA box minus its halo (the half width for split boxes)
   return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR, CL>, C::HW, CW, TY, C::NT, &C::smem_bytes,
-               name, CL};
+               name, CL, C::SWZ};
 }
 
 // interior-kernel variants (WAVE25_INNER_TILE selects one; default first)
@@ -379,14 +380,15 @@ static CUtensorMapL2promotion l2_promotion(int v = -1) {
 
 static wave_status encode3d(CUtensorMap* m, void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                             uint64_t pitch_bytes, uint64_t plane_bytes, uint32_t b0, uint32_t b1,
-                            bool f64 = false, int promo = -1) {
+                            bool f64 = false, int promo = -1, bool swz128 = false) {
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {pitch_bytes, plane_bytes};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = g_encode(m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
                         dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(promo),
+                        CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swz128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, l2_promotion(promo),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(WAVE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return WAVE_OK;
@@ -1563,7 +1565,8 @@ static wave_status encode_buffer(wave_plan* P, int b) {
     const uint32_t TX = KTX(ki), CW = KCW(ki), TY = KTY(ki);
     // cluster kernels load the u window as (2R)-row boxes (multicast halves)
     const uint32_t UH = KCL(ki) > 1 ? 2 * R : TY + 2 * R;
-    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, UH, f64));
+    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, UH, f64, -1,
+                  g_k[P->prec][ki].swz));
     CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY, f64,
                   centre_promo(P, ki, CW)));
   }
