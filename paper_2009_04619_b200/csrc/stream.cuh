@@ -39,7 +39,12 @@ namespace w25 {
 // MODE_FUSED: whole xy plane in one launch, path chosen per warp and plane.
 // MODE_NULL: memory-pattern probe (no stencil; wrong results, diagnostics only).
 // MODE_WALL_ETA: wall kernel reading a stored (user-supplied) eta field.
-enum { MODE_INNER = 0, MODE_WALL = 1, MODE_NULL = 2, MODE_FUSED = 3, MODE_WALL_ETA = 4 };
+// MODE_WALLX / MODE_WALLY: MODE_WALL specialised for the x walls (only the
+// column-constant fast path compiled) / the y walls (row-uniform fast path):
+// half the hot-loop code (ncu: instruction-fetch stalls in the generic wall
+// kernel); other warps fall back to the general path, so any region is correct.
+enum { MODE_INNER = 0, MODE_WALL = 1, MODE_NULL = 2, MODE_FUSED = 3, MODE_WALL_ETA = 4, MODE_WALLX = 5,
+       MODE_WALLY = 6 };
 
 struct Region {
   int x0, x1, y0, y1, z0, z1;   // point box [x0,x1) x [y0,y1) x [z0,z1) (local z)
@@ -654,13 +659,14 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   // registers across the loop they were spilled to local memory around the
   // general path's call, and the LDL latency stalled the wall kernels (§5).
   int wkind = 0;                             // 1: y-wall rows, 2: x-wall columns, 0: general
-  constexpr bool WT = MODE == MODE_WALL || MODE == MODE_FUSED;
+  constexpr bool WALLS = MODE == MODE_WALL || MODE == MODE_WALLX || MODE == MODE_WALLY;
+  constexpr bool WT = WALLS || MODE == MODE_FUSED;
   __shared__ __align__(16) T s_wc[WT ? 4 * CW : 1];   // per column: cg_x, A, B, RN(1/B)
   __shared__ __align__(16) T s_wr[WT ? 4 * TY : 1];   // per row: cg_y, A, B, RN(1/B)
   const int wci = min(NV * lx, CW - NV);     // my first table column (phantom lanes clamp)
   // fused mode: warps touching the x/y PML take the same specialised paths
-  const bool wallw = MODE == MODE_WALL || MODE == MODE_WALL_ETA || (MODE == MODE_FUSED && warp_xy_pml);
-  if (MODE == MODE_WALL || MODE == MODE_FUSED) {
+  const bool wallw = WALLS || MODE == MODE_WALL_ETA || (MODE == MODE_FUSED && warp_xy_pml);
+  if (WALLS || MODE == MODE_FUSED) {
     bool all_dx0 = true, all_dy0 = true;
 #pragma unroll
     for (int r = 0; r < TYT; ++r)
@@ -673,6 +679,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     all_dx0 = __all_sync(0xffffffffu, all_dx0);
     all_dy0 = __all_sync(0xffffffffu, all_dy0);
     wkind = all_dx0 ? 1 : (all_dy0 ? 2 : 0);
+    if (MODE == MODE_WALLX && wkind == 1) wkind = 0;   // (not compiled in this kernel: general path)
+    if (MODE == MODE_WALLY && wkind == 2) wkind = 0;
     // an inner point (d = 0) inside a wall region (the frames of a two-step
     // pair reach 4 or 8 cells into the inner box) takes cg = 0, A = B = 1:
     // ((2u - up) + v (L + 0)) / 1, bitwise the inner update (up to the sign of 0)
@@ -1025,7 +1033,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
         for (int r = 0; r < TYT; ++r) {
           T o[NV];
           T num[NV], Bd[NV], rBd[NV];
-          if (wkind == 1) {
+          if (MODE == MODE_WALLY || (MODE != MODE_WALLX && wkind == 1)) {
             const int ri = ly * TYT + r;
             const T cg = s_wr[ri], Aw = s_wr[TY + ri], Bw = s_wr[2 * TY + ri], rBw = s_wr[3 * TY + ri];
 #pragma unroll
@@ -1184,7 +1192,7 @@ k_mix(const __grid_constant__ CUtensorMap ti_u, const __grid_constant__ CUtensor
     const Region& g0 = M.pw.reg[0];
     const int ncol = g0.ntx * g0.nty;
     const int r = s / ncol;
-    stream_body<TXW, CWW, TYW, 1, MODE_WALL, 1, RA, float, 0>(tw_u, tw_up, tw_v, M.pw,
+    stream_body<TXW, CWW, TYW, 1, MODE_WALLX, 1, RA, float, 0>(tw_u, tw_up, tw_v, M.pw,
                                                              M.pw.reg[r].blk0 + c * ncol + (s - r * ncol));
   }
 }

@@ -107,7 +107,8 @@ static const KInfo* inner_variants(int* n) {
 // x walls: 16 computed columns per tile; 24 + 8 = 32-float (128-B) u boxes
 static const KInfo* wallx_variants(int* n) {
   static const KInfo v[] = {
-      kinfo<24, 16, 128, 1, MODE_WALL, 1, 112>("x24c16x128x1r"),
+      kinfo<24, 16, 128, 1, MODE_WALLX, 1, 112>("x24c16x128x1r"),
+      kinfo<24, 16, 128, 1, MODE_WALL, 1, 112>("x24c16x128x1rg"),     // generic wall body (A/B)
       kinfo<24, 16, 32, 1, MODE_WALL>("x24c16x32x1"),
       kinfo<28, 16, 32, 1, MODE_WALL>("x28c16x32x1"),
       kinfo<24, 16, 64, 1, MODE_WALL, 1, 232>("x24c16x64x1r"),
@@ -127,7 +128,8 @@ static const KInfo* wallx_variants(int* n) {
 
 static const KInfo* wally_variants(int* n) {
   static const KInfo v[] = {
-      kinfo<128, 128, 16, 1, MODE_WALL, 1, 112>("y128x16x1r"),
+      kinfo<128, 128, 16, 1, MODE_WALLY, 1, 112>("y128x16x1r"),
+      kinfo<128, 128, 16, 1, MODE_WALL, 1, 112>("y128x16x1rg"),      // generic wall body (A/B)
       kinfo<64, 64, 8, 1, MODE_WALL, 3>("y64x8x1m3"),
       kinfo<248, 248, 8, 1, MODE_WALL, 1, 112>("y248x8x1r"),
       kinfo<64, 64, 16, 1, MODE_WALL, 2>("y64x16x1m2"),
@@ -157,7 +159,7 @@ static bool is_wall(int ki) { return ki == KI_WALLX || ki == KI_WALLY || ki == K
 static KInfo g_k[2][KI_N];   // [precision: 0 fp32, 1 fp64][kernel kind]
 // the two bodies k_mix instantiates: the default interior and x-wall kernels
 static KInfo mix_inner() { return kinfo<248, 248, 8, 1, MODE_INNER, 1, 112>("248x8x1r"); }
-static KInfo mix_wallx() { return kinfo<24, 16, 128, 1, MODE_WALL, 1, 112>("x24c16x128x1r"); }
+static KInfo mix_wallx() { return kinfo<24, 16, 128, 1, MODE_WALLX, 1, 112>("x24c16x128x1r"); }
 static void* mix_fn() { return (void*)k_mix<248, 8, 24, 16, 128, 112>; }
 static void init_kernels() {
   static bool done = false;
@@ -176,9 +178,9 @@ static void init_kernels() {
   // u box 132 doubles; same ring / warpgroup structure as the fp32 kernels
   g_k[1][KI_INNER] = kinfo<124, 124, 8, 1, MODE_INNER, 1, 112, double>("d124x8x1r");
   {
-    static const KInfo dx[] = {kinfo<24, 16, 64, 1, MODE_WALL, 1, 112, double>("dx24c16x64x1r"),
+    static const KInfo dx[] = {kinfo<24, 16, 64, 1, MODE_WALLX, 1, 112, double>("dx24c16x64x1r"),
                                kinfo<24, 16, 32, 1, MODE_WALL, 1, 0, double>("dx24c16x32x1")};
-    static const KInfo dy[] = {kinfo<64, 64, 16, 1, MODE_WALL, 1, 112, double>("dy64x16x1r"),
+    static const KInfo dy[] = {kinfo<64, 64, 16, 1, MODE_WALLY, 1, 112, double>("dy64x16x1r"),
                                kinfo<32, 32, 8, 1, MODE_WALL, 3, 0, double>("dy32x8x1m3")};
     g_k[1][KI_WALLX] = pick(dx, 2, "WAVE25_DWALLX_TILE");
     g_k[1][KI_WALLY] = pick(dy, 2, "WAVE25_DWALLY_TILE");
