@@ -10,6 +10,8 @@ for cfg in "" "WAVE25_FASTDIV=0"; do
   env $cfg timeout 300 python scripts/prof_kinds.py C3 stream 10 >> gpurun_out/qt_f.txt 2>&1
   env $cfg timeout 300 python scripts/quick_time.py C2 stream 200 >> gpurun_out/qt_f.txt 2>&1
 done
+for t in y248x8x1r y128x16x1rg; do echo "== ytile $t" >> gpurun_out/qt_f.txt; WAVE25_WALLY_TILE=$t timeout 300 python scripts/prof_kinds.py C3 stream 10 >> gpurun_out/qt_f.txt 2>&1; done
+echo "== xtile g" >> gpurun_out/qt_f.txt; WAVE25_WALLX_TILE=x24c16x128x1rg timeout 300 python scripts/prof_kinds.py C3 stream 10 >> gpurun_out/qt_f.txt 2>&1
 echo "== eta" >> gpurun_out/qt_f.txt
 PROF_ETA=1 timeout 300 python scripts/prof_kinds.py C3 stream 6 >> gpurun_out/qt_f.txt 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_stream<(24|128)," -s 2 -c 2 -o gpurun_out/prof_f python scripts/prof_kinds.py C3 stream 1 > gpurun_out/ncu_f.log 2>&1
