@@ -134,10 +134,11 @@ __device__ __forceinline__ f2_t f2_upd_inner(f2_t L, f2_t c, f2_t up, f2_t v) {
 // MUFU, no slow-path call, 3 dependent operations instead of ~10.
 template <typename T>
 __device__ __forceinline__ T div_table(T n, T B, T rB, bool fast) {
-  if (!fast) return div_rn(n, B);
-  if (fabs(n) < T(0x1p-80)) return n == T(0) ? n : div_rn(n, B);
+  if (!fast) return n == T(0) ? n : div_rn(n, B);
   const T q0 = mul_rn(n, rB);
-  return fma_rn(fma_rn(-q0, B, n), rB, q0);
+  const T q = fma_rn(fma_rn(-q0, B, n), rB, q0);
+  if (fabs(n) < T(0x1p-80) && n != T(0)) return div_rn(n, B);
+  return n == T(0) ? n : q;        // +-0 / B = +-0 (the formula would give +0 for -0)
 }
 
 // div_table on the NV points of a lane, straight-line: all fast quotients
@@ -153,14 +154,17 @@ __device__ __forceinline__ void div_table_row(const T* n, const T* B, const T* r
   bool tiny = false;
 #pragma unroll
   for (int c = 0; c < N; ++c) {
-    tiny |= fabs(n[c]) < T(0x1p-80);
+    // zeros (every PML cell the wave has not reached) stay on the straight
+    // line: +-0 / B = +-0 by a select; only tiny non-zero n branch off
+    tiny |= fabs(n[c]) < T(0x1p-80) && n[c] != T(0);
     const T q0 = mul_rn(n[c], rB[c]);
-    q[c] = fma_rn(fma_rn(-q0, B[c], n[c]), rB[c], q0);
+    const T qc = fma_rn(fma_rn(-q0, B[c], n[c]), rB[c], q0);
+    q[c] = n[c] == T(0) ? n[c] : qc;
   }
   if (tiny) {
 #pragma unroll
     for (int c = 0; c < N; ++c)
-      if (fabs(n[c]) < T(0x1p-80)) q[c] = n[c] == T(0) ? n[c] : div_rn(n[c], B[c]);
+      if (fabs(n[c]) < T(0x1p-80) && n[c] != T(0)) q[c] = div_rn(n[c], B[c]);
   }
 }
 
