@@ -590,7 +590,13 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   // ======================= consumer warps ================================
   if (RA > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(RA) : "memory");
   const int lx = (wid % C::WX) * C::LXW + (lane % C::LXW);
-  const int ly = (wid / C::WX) * C::LYW + (lane / C::LXW);
+  // swizzled x-wall stages: a warp's 8 rows are read 2 per quarter-warp (LDS.128
+  // phases of 8 lanes); with the 128-B swizzle (chunk ^= row & 7) rows r and r+1
+  // overlap in 2 of their 4 chunks, rows r and r+4 are disjoint -- so a quarter
+  // takes rows {q, q+4}
+  const int lrow = lane / C::LXW;
+  const int ly = (wid / C::WX) * C::LYW +
+                 ((C::SWZ && C::LYW == 8) ? ((lrow >> 1) | ((lrow & 1) << 2)) : lrow);
   const int gx = cx0 + NV * lx;             // first x of my vector
   const int gy = ty0 + ly * TYT;            // first y of my rows
   // smem offsets (elements) of my vector in row 0 of the tile, u stage / p stage
