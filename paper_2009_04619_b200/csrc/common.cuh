@@ -143,12 +143,22 @@ __device__ __forceinline__ T div_table(T n, T B, T rB, bool fast) {
 
 // div_table on the NV points of a lane, straight-line: all fast quotients
 // first (independent chains interleave), then one rarely taken fix-up for
-// tiny or zero numerators.  Bitwise div_table per element.
+// tiny numerators.  Bitwise div_table per element.  Called by whole warps.
 template <typename T, int N>
 __device__ __forceinline__ void div_table_row(const T* n, const T* B, const T* rB, bool fast, T* q) {
   if (!fast) {
 #pragma unroll
     for (int c = 0; c < N; ++c) q[c] = n[c] == T(0) ? n[c] : div_rn(n[c], B[c]);
+    return;
+  }
+  // a quiet warp (every PML cell the wave has not reached yet: n = +-0 at all
+  // its points) skips the quotients: +-0 / B = +-0 (callers are warp-uniform)
+  bool z = true;
+#pragma unroll
+  for (int c = 0; c < N; ++c) z &= n[c] == T(0);
+  if (__all_sync(0xffffffffu, z)) {
+#pragma unroll
+    for (int c = 0; c < N; ++c) q[c] = n[c];
     return;
   }
   bool tiny = false;
