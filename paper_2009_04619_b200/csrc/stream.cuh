@@ -62,7 +62,8 @@ constexpr int SP = 3;           // u_prev/vdt2 ring stages of the TB2 kernel (di
 #ifndef W25_SP_MAX
 #define W25_SP_MAX 4            // deepest u_prev/vdt2 ring k_stream may use (A/B builds: -DW25_SP_MAX=3)
 #endif
-constexpr int W25_MAX_W = 512;  // largest PML width (the shared eta table holds 3 (w + 2) entries)
+constexpr int W25_MAX_W = 256;  // largest PML width (the shared tables hold 4 (w + 2) entries; 256 leaves the
+                                // x walls room for a 4-stage u_prev/vdt2 ring)
 constexpr int W25_SMEM_BUDGET = 232448 - 4096;   // 227 KB opt-in limit minus static shared memory
 
 struct StreamParams {
@@ -170,13 +171,16 @@ struct StreamCfg {
   static constexpr int P_STAGE = CW * TY;                   // elements per u_prev / vdt2 stage
   // stored-eta kernels (ETA): an fp32 eta box of (CW + 8) x (TY + 2) per u_prev
   // stage -- the tile with a 1-cell y halo and a 4-cell (16-B) x halo
+  // (see SWZ below: 128-B-row u boxes are loaded swizzled and need a 1024-B aligned layout)
+  static constexpr bool SWZ_ = NH == 1 && (HW + 2 * R) * (int)sizeof(T) == 128 &&
+                               ((HW + 2 * R) * (TY + 2 * R) * (int)sizeof(T)) % 1024 == 0;
   static constexpr int EW = CW + 8;
   static constexpr int E_STAGE = ETA ? (EW * (TY + 2) + 31) / 32 * 32 : 0;  // floats (stages 128-B aligned)
   // u_prev / vdt2 ring depth: as deep as shared memory allows (3..W25_SP_MAX
   // stages), so more of those two streams is in flight per SM
   static constexpr int fits_(int n) {
-    return (SU * U_STAGE + 2 * n * P_STAGE) * (int)sizeof(T) + n * E_STAGE * 4 + 2 * (SU + n) * 8 +
-               4 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
+    return (SWZ_ ? 1024 : 0) + (SU * U_STAGE + 2 * n * P_STAGE) * (int)sizeof(T) + n * E_STAGE * 4 +
+               2 * (SU + n) * 8 + 4 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
   }
   static constexpr int SPN = (W25_SP_MAX >= 5 && fits_(5)) ? 5 : (W25_SP_MAX >= 4 && fits_(4)) ? 4 : 3;
   static constexpr int E_OFF = (SU * U_STAGE + 2 * SPN * P_STAGE) * (int)sizeof(T);    // bytes (eta ring)
@@ -186,7 +190,7 @@ struct StreamCfg {
   // floats) are loaded with the TMA 128-B swizzle: a float4 column read across
   // the 8 rows of a warp would otherwise hit the same 16 banks (2 wavefronts
   // per 128 B); swizzled stages need 1024-B alignment
-  static constexpr bool SWZ = NH == 1 && SW * (int)sizeof(T) == 128 && (U_HALF * (int)sizeof(T)) % 1024 == 0;
+  static constexpr bool SWZ = SWZ_;
   static constexpr int ALIGN_PAD = SWZ ? 1024 : 0;
   static size_t smem_bytes(int w) { return ALIGN_PAD + TAB_OFF + 4 * (w + 2) * sizeof(T); }
   static_assert(CW % 4 == 0 && CW <= TX && TX % 4 == 0, "tile widths");

@@ -1,0 +1,15 @@
+#!/bin/bash
+# round 2: x-wall quarter-warp row pairing + quiet-warp skip: timing, wall ncu, correctness subset
+cd $GRAFT_REPO_ROOT
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+for cfg in "" "WAVE25_FASTDIV=0"; do
+  echo "== $cfg" >> gpurun_out/qt_i.txt
+  env $cfg timeout 300 python scripts/quick_time.py C3 stream 100 >> gpurun_out/qt_i.txt 2>&1
+  env $cfg timeout 300 python scripts/prof_kinds.py C3 stream 10 >> gpurun_out/qt_i.txt 2>&1
+  env $cfg timeout 300 python scripts/quick_time.py C2 stream 200 >> gpurun_out/qt_i.txt 2>&1
+  env $cfg timeout 300 python scripts/prof_kinds.py C2 stream 20 >> gpurun_out/qt_i.txt 2>&1
+done
+timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled -k 'regex:k_stream<\(int\)(24|128),' -s 2 -c 2 -o gpurun_out/prof_i python scripts/prof_kinds.py C3 stream 1 > gpurun_out/ncu_i.log 2>&1
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_eta.py tests/test_gpu_fp64.py -m gpu -x -q -p no:cacheprovider > gpurun_out/t_i.log 2>&1
+echo "rc=$?" >> gpurun_out/t_i.log
+echo done
