@@ -102,7 +102,8 @@ typedef enum { WAVE_PREC_FP32 = 0, WAVE_PREC_FP64 = 1 } wave_precision;
  *              THIS plan; x innermost.  nz = planes of this rank's z-slab
  *              (= nz_global on one GPU).                         all >= 1
  *  pml_width   w, uniform on all six faces;
- *              0 <= 2w < min(nx, ny, nz_global)
+ *              0 <= 2w < min(nx, ny, nz_global), w <= 256
+ *              (the kernels' shared PML tables hold 4 (w + 2) entries)
  *  kernel      wave_kernel
  *  hx, hy, hz  spacing (m), > 0 (per-axis, R1)
  *  dt          time step (s) as the fp32 value used; > 0, or 0 = automatic
@@ -146,7 +147,11 @@ typedef struct {
     int64_t elems_vdt2;   /* floats in the vdt2 buffer                                    */
     int64_t align_bytes;  /* 128                                                          */
     int64_t elem_bytes;   /* 4 (fp32 plans) or 8 (fp64 plans): buffer element size        */
-    int64_t origin;       /* elements before the layout's first element (0 or < 128 B)     */
+    int64_t origin;       /* elements before the layout's first element: the 128-B line
+                             shift, plus one pad row when `seam` is set                   */
+    int64_t seam;         /* 1: the x walls run as seams (both walls of adjacent rows in
+                             one line); the buffers then also end with one
+                             pad row; never written, read only into masked lanes          */
 } wave_layout_info;
 
 /* One region of the paper's 7-region decomposition (PAPER.md L342-356,

@@ -53,7 +53,7 @@ class WaveDesc(ctypes.Structure):
 class WaveLayout(ctypes.Structure):
     _fields_ = [("pitch_x", ctypes.c_int64), ("ghost_z", ctypes.c_int64), ("planes", ctypes.c_int64),
                 ("elems_u", ctypes.c_int64), ("elems_vdt2", ctypes.c_int64), ("align_bytes", ctypes.c_int64),
-                ("elem_bytes", ctypes.c_int64), ("origin", ctypes.c_int64)]
+                ("elem_bytes", ctypes.c_int64), ("origin", ctypes.c_int64), ("seam", ctypes.c_int64)]
 
 
 class WaveRegion(ctypes.Structure):

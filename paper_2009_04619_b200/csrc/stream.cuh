@@ -43,8 +43,14 @@ namespace w25 {
 // column-constant fast path compiled) / the y walls (row-uniform fast path):
 // half the hot-loop code (ncu: instruction-fetch stalls in the generic wall
 // kernel); other warps fall back to the general path, so any region is correct.
+// MODE_SEAM: the two x walls as "seams" -- seam t = [right wall of row t-1 |
+// left wall of row t], 2w contiguous points of one 128-B line (fp32, w = 16,
+// rows of exactly nx elements, the layout's origin shift).  The
+// region's x range is [R, R + 2w) and y range the seam index t in [0, ny + 1)
+// of seam tensor maps whose column 0 is x = nx - w - R of row t - 1.  Only the
+// column-constant fast path is compiled (like MODE_WALLX).
 enum { MODE_INNER = 0, MODE_WALL = 1, MODE_NULL = 2, MODE_FUSED = 3, MODE_WALL_ETA = 4, MODE_WALLX = 5,
-       MODE_WALLY = 6 };
+       MODE_WALLY = 6, MODE_SEAM = 7 };
 
 struct Region {
   int x0, x1, y0, y1, z0, z1;   // point box [x0,x1) x [y0,y1) x [z0,z1) (local z)
@@ -603,6 +609,15 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
                  ((C::SWZ && C::LYW == 8) ? ((lrow >> 1) | ((lrow & 1) << 2)) : lrow);
   const int gx = cx0 + NV * lx;             // first x of my vector
   const int gy = ty0 + ly * TYT;            // first y of my rows
+  // the global point coordinates of my vector: (px + c, py + r); for seams the
+  // right-wall half (seam columns [0, w)) lies on row t - 1 at x = nx - w + col,
+  // the left-wall half on row t at x = col - w
+  constexpr bool SEAM = MODE == MODE_SEAM;
+  static_assert(!SEAM || (TYT == 1 && true), "seam tiles: one row per lane");
+  const int scol = gx - G.x0;
+  const bool sright = SEAM && scol < P.w;
+  const int px = SEAM ? (sright ? P.nx - P.w + scol : scol - P.w) : gx;
+  const int py = SEAM ? gy - (sright ? 1 : 0) : gy;
   // smem offsets (elements) of my vector in row 0 of the tile, u stage / p stage
   const int hf = (NV * lx) / C::HW;         // which half box (warp-uniform)
   // element offset of logical window row l (0 .. TY+2R-1 of the u box) at my
@@ -638,7 +653,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
 #pragma unroll
     for (int c = 0; c < NV; ++c) {
       const int x = gx + c, y = gy + r;
-      if (x >= G.x0 && x < G.x1 && y >= G.y0 && y < G.y1) mask |= 1u << (r * NV + c);
+      if (x >= G.x0 && x < G.x1 && y >= G.y0 && y < G.y1 && (!SEAM || (py + r >= 0 && py + r < P.ny)))
+        mask |= 1u << (r * NV + c);
     }
   if (NV * lx >= CW) mask = 0;               // phantom lane beyond the computed width
   const bool full = mask == (TYT * NV == 32 ? 0xffffffffu : ((1u << (TYT * NV)) - 1u));
@@ -669,7 +685,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   // registers across the loop they were spilled to local memory around the
   // general path's call, and the LDL latency stalled the wall kernels (§5).
   int wkind = 0;                             // 1: y-wall rows, 2: x-wall columns, 0: general
-  constexpr bool WALLS = MODE == MODE_WALL || MODE == MODE_WALLX || MODE == MODE_WALLY;
+  constexpr bool WALLS = MODE == MODE_WALL || MODE == MODE_WALLX || MODE == MODE_WALLY || MODE == MODE_SEAM;
   constexpr bool WT = WALLS || MODE == MODE_FUSED;
   __shared__ __align__(16) T s_wc[WT ? 4 * CW : 1];   // per column: cg_x, A, B, RN(1/B)
   __shared__ __align__(16) T s_wr[WT ? 4 * TY : 1];   // per row: cg_y, A, B, RN(1/B)
@@ -683,13 +699,13 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
 #pragma unroll
       for (int c = 0; c < NV; ++c)
         if ((mask >> (r * NV + c)) & 1u) {
-          all_dx0 &= dist1(gx + c, P.nx, P.w) == 0;
-          all_dy0 &= dist1(gy + r, P.ny, P.w) == 0;
+          all_dx0 &= dist1(px + c, P.nx, P.w) == 0;
+          all_dy0 &= dist1(py + r, P.ny, P.w) == 0;
         }
     all_dx0 = __all_sync(0xffffffffu, all_dx0);
     all_dy0 = __all_sync(0xffffffffu, all_dy0);
     wkind = all_dx0 ? 1 : (all_dy0 ? 2 : 0);
-    if (MODE == MODE_WALLX && wkind == 1) wkind = 0;   // (not compiled in this kernel: general path)
+    if ((MODE == MODE_WALLX || SEAM) && wkind == 1) wkind = 0;   // (not compiled in this kernel: general path)
     if (MODE == MODE_WALLY && wkind == 2) wkind = 0;
     // an inner point (d = 0) inside a wall region (the frames of a two-step
     // pair reach 4 or 8 cells into the inner box) takes cg = 0, A = B = 1:
@@ -710,10 +726,10 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     if (ly == 0 && NV * lx < CW) {           // one writer per tile column
 #pragma unroll
       for (int c = 0; c < NV; ++c) {
-        const int dx = dist1(gx + c, P.nx, P.w);
+        const int dx = dist1(px + c, P.nx, P.w);
         s_wc[NV * lx + c] =
             dx == 0 ? T(0)
-                    : mul_rn(sub_rn(stab[dist1(gx + c + 1, P.nx, P.w)], stab[dist1(gx + c - 1, P.nx, P.w)]),
+                    : mul_rn(sub_rn(stab[dist1(px + c + 1, P.nx, P.w)], stab[dist1(px + c - 1, P.nx, P.w)]),
                              PG.i2hx);
         s_wc[CW + NV * lx + c] = stab[TABN + dx];
         s_wc[2 * CW + NV * lx + c] = stab[2 * TABN + dx];
@@ -723,8 +739,17 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     // consumer warps only (the producer warps have left): named barrier 1
     asm volatile("bar.sync 1, %0;" ::"r"(C::NWC * 32) : "memory");
   }
+  // (seams: both halves of seam t sit at t * pitch + gx - (x0 + w) when a row
+  // is exactly nx = pitch elements long; the host guarantees that)
+  const int64_t sadj = SEAM ? -(int64_t)(G.x0 + P.w) : 0;
   T* optr = static_cast<T*>((PAIR && role == 2) ? P.out2 : P.out) + (int64_t)(zs + R) * P.plane +
-            (int64_t)gy * P.pitch + gx;
+            (int64_t)gy * P.pitch + gx + sadj;
+  // seams: the window row of my half that is not a grid row (row -1 of the
+  // right half, row ny of the left half) must read as 0 (the Dirichlet fringe),
+  // and the x neighbours across the seam boundary too
+  const int yzero = !SEAM ? -100 : (sright ? R - gy : P.ny - gy + R);   // window index jj, or out of range
+  const bool xr_zero = SEAM && scol + NV == P.w;   // right half's last vector: x+1.. beyond nx-1
+  const bool xl_zero = SEAM && scol == P.w;        // left half's first vector: x-1.. below 0
   // PAIR: the source cell is injected by the block that computes it (step 1
   // adds inc[n], step 2 inc[n+1]); -1 if not in my vector rows
   int src_r = -1, src_c = 0;
@@ -798,6 +823,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       for (int jj = 0; jj < TYT + 2 * R; ++jj) {
         if (jj >= R && jj < R + TYT) Y[jj] = q[sc][jj - R];
         else Y[jj] = ldv(su + sc * C::U_STAGE + (C::SWZ ? uzc(jj) : yo(jj)));
+        if (SEAM && jj == yzero) Y[jj] = V{};
       }
       // x neighbours: KX vectors on each side of the centre vector
       V XL[TYT][KX], XR[TYT][KX];
@@ -815,6 +841,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
             XL[r][k] = ldv(S + r * C::SW - (KX - k) * NV);
             XR[r][k] = ldv(S + r * C::SW + (k + 1) * NV);
           }
+          if (SEAM && xl_zero) XL[r][k] = V{};
+          if (SEAM && xr_zero) XR[r][k] = V{};
         }
       T X[TYT][(2 * KX + 1) * NV];           // x-4.. of my points, centre at XC
 #pragma unroll
@@ -1043,7 +1071,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
         for (int r = 0; r < TYT; ++r) {
           T o[NV];
           T num[NV], Bd[NV], rBd[NV];
-          if (MODE == MODE_WALLY || (MODE != MODE_WALLX && wkind == 1)) {
+          if (MODE == MODE_WALLY || (MODE != MODE_WALLX && MODE != MODE_SEAM && wkind == 1)) {
             const int ri = ly * TYT + r;
             const T cg = s_wr[ri], Aw = s_wr[TY + ri], Bw = s_wr[2 * TY + ri], rBw = s_wr[3 * TY + ri];
 #pragma unroll
@@ -1076,7 +1104,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
 #pragma unroll
           for (int c = 0; c < NV; ++c) { xpa[c] = X[r][XC + c + 1]; xma[c] = X[r][XC + c - 1]; }
           res[r] = pml_row_call<T>(vmake<T>(L[r]), Y[R + r], upv[r], vv[r], vmake<T>(xpa), vmake<T>(xma),
-                                   Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], gx, gy + r,
+                                   Y[R + r + 1], Y[R + r - 1], q[(s + 5) % 9][r], q[(s + 3) % 9][r], px, py + r,
                                    kg, PG, stab, P.fastdiv != 0);
         }
       }
@@ -1120,7 +1148,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
         if (side == 0 && z < R && P.rlo) rbase = static_cast<T*>(P.rlo) + (int64_t)z * P.plane;
         if (side == 1 && z >= P.nzl - R && P.rhi) rbase = static_cast<T*>(P.rhi) + (int64_t)(z - (P.nzl - R)) * P.plane;
         if (rbase) {
-          T* rp = rbase + (int64_t)gy * P.pitch + gx;
+          T* rp = rbase + (int64_t)gy * P.pitch + gx + sadj;
           if (full) {
 #pragma unroll
             for (int r = 0; r < TYT; ++r) *reinterpret_cast<V*>(rp + r * P.pitch) = res[r];

@@ -152,9 +152,12 @@ static KInfo pick(const KInfo* v, int n, const char* env) {
 
 // KI_WALLX_E / KI_WALLY_E: the wall kernels of the stored-eta mode
 // KI_PAIR: the two-step-through-L2 interior kernel
+// KI_SEAM: both x walls as seams (MODE_SEAM)
 enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_WALLX_E = 4, KI_WALLY_E = 5, KI_PAIR = 6,
-       KI_N = 7 };
-static bool is_wall(int ki) { return ki == KI_WALLX || ki == KI_WALLY || ki == KI_WALLX_E || ki == KI_WALLY_E; }
+       KI_SEAM = 7, KI_N = 8 };
+static bool is_wall(int ki) {
+  return ki == KI_WALLX || ki == KI_WALLY || ki == KI_WALLX_E || ki == KI_WALLY_E || ki == KI_SEAM;
+}
 
 static KInfo g_k[2][KI_N];   // [precision: 0 fp32, 1 fp64][kernel kind]
 // the two bodies k_mix instantiates: the default interior and x-wall kernels
@@ -192,6 +195,12 @@ static void init_kernels() {
   g_k[0][KI_PAIR] = kinfo<248, 248, 8, 1, MODE_INNER, 1, 112, float, 1>("pair248x8x1r");
   g_k[1][KI_PAIR] = kinfo<124, 124, 8, 1, MODE_INNER, 1, 112, double, 1>("dpair124x8x1r");
   g_k[1][KI_FUSED] = kinfo<64, 64, 8, 1, MODE_FUSED, 2, 0, double>("dfused64x8x1");
+  {
+    static const KInfo sv[] = {kinfo<32, 32, 64, 1, MODE_SEAM, 1, 112>("seam32x64r"),
+                               kinfo<32, 32, 32, 1, MODE_SEAM, 2>("seam32x32")};
+    g_k[0][KI_SEAM] = pick(sv, 2, "WAVE25_SEAM_TILE");
+  }
+  g_k[1][KI_SEAM] = g_k[1][KI_WALLX];   // (fp32 only; fp64 plans never build seam launches)
   done = true;
 }
 #define KTX(ki) (g_k[P->prec][ki].tx)
@@ -274,7 +283,7 @@ struct wave_plan {
   Stats* stats_d = nullptr;
   // launch plans
   Maps maps[KI_N];
-  int occ[KI_N] = {1, 1, 1, 1, 1, 1, 1};
+  int occ[KI_N] = {1, 1, 1, 1, 1, 1, 1, 1};
   bool fused = false;                // WAVE25_FUSED=1: one launch, per-warp paths (measured slower)
   int pf = 1;                        // L2 prefetch distance (WAVE25_PF), measured best
   int wall_pf = -1;                  // wall kernels' L2 prefetch distance (WAVE25_WALL_PF; -1 = pf)
@@ -300,6 +309,7 @@ struct wave_plan {
   int xwall_extra = 0;               // WAVE25_XWALL_EXTRA: inner columns computed by the x-wall kernel
   bool xinter = true;                // WAVE25_XINTER=0: x-wall launch region-major instead of left/right interleaved
   bool fastdiv_on = true;            // WAVE25_FASTDIV=0: IEEE division in the PML updates (A/B)
+  bool seam_on = true;               // WAVE25_SEAM=0: the x walls as two regions instead of seams (A/B)
   bool fastdiv = false;              // table division verified bitwise for this plan (check_fastdiv)
   bool walls_last = false;           // WAVE25_WALLS_LAST: enqueue the wall kernels after the interior
   int mix = 0;                       // WAVE25_MIX=1/2: interior + x walls as one grid (k_mix, §5i; measured slower)
@@ -455,8 +465,16 @@ static void make_layout(const wave_desc& d, wave_layout_info* L) {
     const int64_t sb = ((128 - (d.pml_width * L->elem_bytes) % 128) % 128) / 16 * 16;
     L->origin = sb / L->elem_bytes;
   }
-  L->elems_u = L->origin + L->planes * d.ny * L->pitch_x;
-  L->elems_vdt2 = L->origin + d.nz * d.ny * L->pitch_x;
+  // seams (MODE_SEAM): fp32, w = 16 (one 128-B line = both walls), rows of
+  // exactly nx elements; a seam view reads row -1 of the first plane and row ny
+  // of the last one, so one pad row is kept before and after every buffer
+  L->seam = d.precision == WAVE_PREC_FP32 && d.pml_width == 16 && L->pitch_x == d.nx && L->origin * 4 == 64 &&
+            d.ny > 2 * d.pml_width && d.nx > 2 * d.pml_width;
+  static const bool no_seam = getenv("WAVE25_NO_SEAM") && atoi(getenv("WAVE25_NO_SEAM")) != 0;   // A/B only
+  if (no_seam) L->seam = 0;
+  if (L->seam) L->origin += L->pitch_x;
+  L->elems_u = L->origin + L->planes * d.ny * L->pitch_x + (L->seam ? L->pitch_x : 0);
+  L->elems_vdt2 = L->origin + d.nz * d.ny * L->pitch_x + (L->seam ? L->pitch_x : 0);
 }
 
 // fp64 plans: every constant in fp64, never rounded to fp32
@@ -557,6 +575,13 @@ struct ZRange { int z0, z1; };
 static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 4>>& xy,
                         const std::vector<ZRange>& zr, std::vector<Launch>* out);
 
+// x walls as seams (MODE_SEAM): the layout reserved the pad rows (fp32, w = 16,
+// rows of exactly nx), and no mode that shapes the x walls differently is on
+static bool seam_active(const wave_plan* P) {
+  return P->L.seam && P->prec == 0 && !P->eta_on && !P->fused && !P->xfuse && P->xwall_extra == 0 && P->seam_on &&
+         P->d.kernel == WAVE_KERNEL_STREAM;
+}
+
 static wave_status build_launches(wave_plan* P) {
   const int nx = (int)P->d.nx, ny = (int)P->d.ny, nz = (int)P->d.nz, w = P->d.pml_width;
   std::vector<ZRange> all = {{0, nz}}, edges, inter;
@@ -602,7 +627,10 @@ static wave_status build_launches(wave_plan* P) {
       // x-wall width (>= w: extra inner columns; not with a stored eta, whose
       // interior launch keeps the inner xy footprint)
       const int xw = w + (P->eta_on ? 0 : P->xwall_extra);
-      add_regions(P, kx, {{0, xw, 0, ny}, {nx - xw, nx, 0, ny}}, *sets[s], &P->launches[s]);
+      if (seam_active(P))   // both x walls as seams t = 0..ny (x range [R, R + 2w) of the seam views)
+        add_regions(P, KI_SEAM, {{R, R + 2 * w, 0, ny + 1}}, *sets[s], &P->launches[s]);
+      else
+        add_regions(P, kx, {{0, xw, 0, ny}, {nx - xw, nx, 0, ny}}, *sets[s], &P->launches[s]);
       add_regions(P, ky, {{xw, nx - xw, 0, w}, {xw, nx - xw, ny - w, ny}}, *sets[s], &P->launches[s]);
     }
   }
@@ -1419,6 +1447,7 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_WALL_CZ")) P->wall_cz = atoi(e);
   if (const char* e = getenv("WAVE25_XINTER")) P->xinter = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_FASTDIV")) P->fastdiv_on = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_SEAM")) P->seam_on = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_PEER_TIMEOUT_S")) P->peer_timeout_s = std::max(1e-3, atof(e));
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
   if (const char* e = getenv("WAVE25_WALLS_LAST")) P->walls_last = atoi(e) != 0;
@@ -1565,6 +1594,15 @@ static wave_status encode_buffer(wave_plan* P, int b) {
   const bool f64 = P->prec == 1;
   for (int ki = 0; ki < KI_N; ++ki) {
     const uint32_t TX = KTX(ki), CW = KCW(ki), TY = KTY(ki);
+    if (ki == KI_SEAM) {
+      // seam views: column 0 = x (nx - w - R) of row t - 1, t = 0..ny (ny + 1 seams)
+      if (!P->L.seam || P->prec) continue;
+      const int w = P->d.pml_width;
+      float* sb = eo(P, P->buf[b], P->d.nx - w - R - P->L.pitch_x);
+      CKST(encode3d(&P->maps[ki].u[b], sb, 2 * w + 2 * R, P->d.ny + 1, P->L.planes, pb, plb, TX + 2 * R, TY + 2 * R));
+      CKST(encode3d(&P->maps[ki].up[b], sb, 2 * w + 2 * R, P->d.ny + 1, P->L.planes, pb, plb, CW, TY));
+      continue;
+    }
     // cluster kernels load the u window as (2R)-row boxes (multicast halves)
     const uint32_t UH = KCL(ki) > 1 ? 2 * R : TY + 2 * R;
     CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, UH, f64, -1,
@@ -1605,9 +1643,17 @@ wave_status wave_plan_bind(wave_plan* P, float* u0, float* u1, float* vdt2, void
   CK(cudaMemsetAsync(P->vdt2_base, 0, P->L.elems_vdt2 * P->esz, s));
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
   const uint64_t pb = P->L.pitch_x * P->esz, plb = pb * P->d.ny;
-  for (int ki = 0; ki < KI_N; ++ki)
+  for (int ki = 0; ki < KI_N; ++ki) {
+    if (ki == KI_SEAM) {
+      if (!P->L.seam || P->prec) continue;
+      const int w = P->d.pml_width;
+      CKST(encode3d(&P->maps[ki].v, eo(P, vdt2, P->d.nx - w - R - P->L.pitch_x), 2 * w + 2 * R, P->d.ny + 1,
+                    P->d.nz, pb, plb, KCW(ki), KTY(ki)));
+      continue;
+    }
     CKST(encode3d(&P->maps[ki].v, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, KCW(ki), KTY(ki), P->prec == 1,
                   centre_promo(P, ki, KCW(ki))));
+  }
   if (P->d.kernel == WAVE_KERNEL_TB2) {
     CKST(encode3d(&P->t2maps.v1, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, P->t2.tx + 2 * R, P->t2.ty + 2 * R));
     CKST(encode3d(&P->t2maps.v2, vdt2, P->d.nx, P->d.ny, P->d.nz, pb, plb, P->t2.tx, P->t2.ty));
@@ -2080,7 +2126,9 @@ float wave_get_dt(const wave_plan* P) { return P ? P->dt : 0.f; }
 // measurement kind of a kernel (the fused launch is the interior kind: it is
 // the dominant kernel and covers every point)
 static int kk_of(int ki) {
-  return ki == KI_FUSED ? WAVE_KK_INTERIOR : ki == KI_WALLX_E ? WAVE_KK_XWALLS : ki == KI_WALLY_E ? WAVE_KK_YWALLS : ki;
+  return ki == KI_FUSED ? WAVE_KK_INTERIOR
+         : (ki == KI_WALLX_E || ki == KI_SEAM) ? WAVE_KK_XWALLS
+         : ki == KI_WALLY_E ? WAVE_KK_YWALLS : ki;
 }
 
 static int64_t region_points(const std::vector<Launch>& Ls, int kind) {
@@ -2089,7 +2137,9 @@ static int64_t region_points(const std::vector<Launch>& Ls, int kind) {
     if (kk_of(L.ki) == kind)
       for (int r = 0; r < L.p.nreg; ++r) {
         const Region& g = L.p.reg[r];
-        n += (int64_t)(g.x1 - g.x0) * (g.y1 - g.y0) * (g.z1 - g.z0);
+        // (seams t = 0..ny: the right half of seam 0 and the left half of seam ny are not points)
+        const int64_t rows = L.ki == KI_SEAM ? (int64_t)(g.y1 - g.y0 - 1) : (int64_t)(g.y1 - g.y0);
+        n += (int64_t)(g.x1 - g.x0) * rows * (g.z1 - g.z0);
       }
   return n;
 }

@@ -117,6 +117,9 @@ def reference(scen, phases):
     (("RAGGED", {}), [0, 24, 28, 53], [(15, 73)]),
     # 4 ranks, two adjacent R-plane slabs (a thin slab's neighbour is thin too)
     (("RAGGED", {}), [0, 24, 28, 32, 53], [(13, 77)]),
+    # the seam x walls (w = 16, rows of exactly nx: DESIGN.md §5a) on slabs: 3
+    # ranks, a 4-plane middle slab holding the source (C1: 64^3, centre source)
+    (("C1", {}), [0, 30, 34, 64], [(17, 79)]),
     # 4 ranks, strong-scaling geometry: thin slabs, the z-PML (w=5) only on the
     # end ranks, the source on plane 20 = the first plane of a 7-plane slab (an
     # edge plane of both of its faces: mirrored into both neighbours)
