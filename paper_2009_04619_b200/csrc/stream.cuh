@@ -748,6 +748,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   // right half, row ny of the left half) must read as 0 (the Dirichlet fringe),
   // and the x neighbours across the seam boundary too
   const int yzero = !SEAM ? -100 : (sright ? R - gy : P.ny - gy + R);   // window index jj, or out of range
+  // (only warps within R seams of either end mask: a warp-uniform branch)
+  const bool yzero_warp = SEAM && __any_sync(0xffffffffu, yzero >= 0 && yzero < TYT + 2 * R);
   const bool xr_zero = SEAM && scol + NV == P.w;   // right half's last vector: x+1.. beyond nx-1
   const bool xl_zero = SEAM && scol == P.w;        // left half's first vector: x-1.. below 0
   // PAIR: the source cell is injected by the block that computes it (step 1
@@ -823,7 +825,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       for (int jj = 0; jj < TYT + 2 * R; ++jj) {
         if (jj >= R && jj < R + TYT) Y[jj] = q[sc][jj - R];
         else Y[jj] = ldv(su + sc * C::U_STAGE + (C::SWZ ? uzc(jj) : yo(jj)));
-        if (SEAM && jj == yzero) Y[jj] = V{};
+        if (SEAM && yzero_warp && jj == yzero) Y[jj] = V{};
       }
       // x neighbours: KX vectors on each side of the centre vector
       V XL[TYT][KX], XR[TYT][KX];
