@@ -309,7 +309,7 @@ struct wave_plan {
   int xwall_extra = 0;               // WAVE25_XWALL_EXTRA: inner columns computed by the x-wall kernel
   bool xinter = true;                // WAVE25_XINTER=0: x-wall launch region-major instead of left/right interleaved
   bool fastdiv_on = true;            // WAVE25_FASTDIV=0: IEEE division in the PML updates (A/B)
-  bool seam_on = true;               // WAVE25_SEAM=0: the x walls as two regions instead of seams (A/B)
+  bool seam_on = false;              // WAVE25_SEAM=1: the x walls as seams (measured slower; A/B)
   bool fastdiv = false;              // table division verified bitwise for this plan (check_fastdiv)
   bool walls_last = false;           // WAVE25_WALLS_LAST: enqueue the wall kernels after the interior
   int mix = 0;                       // WAVE25_MIX=1/2: interior + x walls as one grid (k_mix, §5i; measured slower)

@@ -403,7 +403,8 @@ for name in ("RAGGED", "C1"):
     {"WAVE25_INNER_TILE": "248x8x1rc2"}, {"WAVE25_INNER_TILE": "248x8x1rc4"},
     {"WAVE25_FASTDIV": "0"}, {"WAVE25_NO_ORIGIN": "1"}, {"WAVE25_XINTER": "0"},
     {"WAVE25_WALLX_TILE": "x24c16x128x1rg"}, {"WAVE25_WALLY_TILE": "y128x16x1rg"},
-    {"WAVE25_SEAM": "0"}, {"WAVE25_NO_SEAM": "1"}, {"WAVE25_SEAM_TILE": "seam32x32"},
+    {"WAVE25_SEAM": "1"}, {"WAVE25_SEAM": "1", "WAVE25_NO_SEAM": "1"},
+    {"WAVE25_SEAM": "1", "WAVE25_SEAM_TILE": "seam32x32"},
     {"WAVE25_FUSED": "1", "WAVE25_FUSED_TILE": "fused128x8x1"},
     {"WAVE25_ABLATION": "gmem_32x4x1"}, {"WAVE25_ABLATION": "gmem_8x8x8"}, {"WAVE25_ABLATION": "smem_u"},
     {"WAVE25_ABLATION": "st_smem_32x16"}, {"WAVE25_ABLATION": "st_reg_shft_32x16"},

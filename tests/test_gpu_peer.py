@@ -110,22 +110,25 @@ def reference(scen, phases):
     return one_plan(s, steps, synth.random_state(sh, seed), synth.random_state(sh, seed + 1), wl)
 
 
-@pytest.mark.parametrize("scen,bounds,phases", [
+@pytest.mark.parametrize("scen,bounds,phases,env", [
     # 3 ranks, the middle slab 5 planes (< 2R): both neighbours mapped over IPC
-    (("RAGGED", {}), [0, 20, 25, 53], [(19, 71)]),
+    (("RAGGED", {}), [0, 20, 25, 53], [(19, 71)], {}),
     # 3 ranks, middle slab of exactly R planes (every plane an edge of both faces)
-    (("RAGGED", {}), [0, 24, 28, 53], [(15, 73)]),
+    (("RAGGED", {}), [0, 24, 28, 53], [(15, 73)], {}),
     # 4 ranks, two adjacent R-plane slabs (a thin slab's neighbour is thin too)
-    (("RAGGED", {}), [0, 24, 28, 32, 53], [(13, 77)]),
-    # the seam x walls (w = 16, rows of exactly nx: DESIGN.md §5a) on slabs: 3
+    (("RAGGED", {}), [0, 24, 28, 32, 53], [(13, 77)], {}),
+    # the seam x walls (opt-in WAVE25_SEAM=1; w = 16, rows of exactly nx: DESIGN.md §5a) on slabs: 3
     # ranks, a 4-plane middle slab holding the source (C1: 64^3, centre source)
-    (("C1", {}), [0, 30, 34, 64], [(17, 79)]),
+    (("C1", {}), [0, 30, 34, 64], [(17, 79)], {"WAVE25_SEAM": "1"}),
+    (("C1", {}), [0, 30, 34, 64], [(17, 79)], {}),
     # 4 ranks, strong-scaling geometry: thin slabs, the z-PML (w=5) only on the
     # end ranks, the source on plane 20 = the first plane of a 7-plane slab (an
     # edge plane of both of its faces: mirrored into both neighbours)
-    (("RAGGED", dict(nz=48, w=5, src=(35, 22, 20))), [0, 14, 20, 27, 48], [(21, 75)]),
+    (("RAGGED", dict(nz=48, w=5, src=(35, 22, 20))), [0, 14, 20, 27, 48], [(21, 75)], {}),
 ])
-def test_peer_processes_bitwise(scen, bounds, phases):
+def test_peer_processes_bitwise(scen, bounds, phases, env, monkeypatch):
+    for k, v in env.items():       # (inherited by the spawned ranks; the reference plan reads it too)
+        monkeypatch.setenv(k, v)
     got, gotp = run_world(scen, bounds, phases)
     ref, refp = reference(scen, phases)
     assert np.array_equal(got, ref) and np.array_equal(gotp, refp)
