@@ -49,8 +49,11 @@ namespace w25 {
 // region's x range is [R, R + 2w) and y range the seam index t in [0, ny + 1)
 // of seam tensor maps whose column 0 is x = nx - w - R of row t - 1.  Only the
 // column-constant fast path is compiled (like MODE_WALLX).
+// MODE_INNER_EW: MODE_INNER whose producer warpgroup also computes the PML
+// walls -- two "wall warps" stream 16 x 8 wall tiles through their own small
+// TMA ring while the consumer warps stream the interior tile.
 enum { MODE_INNER = 0, MODE_WALL = 1, MODE_NULL = 2, MODE_FUSED = 3, MODE_WALL_ETA = 4, MODE_WALLX = 5,
-       MODE_WALLY = 6, MODE_SEAM = 7 };
+       MODE_WALLY = 6, MODE_SEAM = 7, MODE_INNER_EW = 8 };
 
 struct Region {
   int x0, x1, y0, y1, z0, z1;   // point box [x0,x1) x [y0,y1) x [z0,z1) (local z)
@@ -60,6 +63,7 @@ struct Region {
 };
 
 constexpr int MAX_REGIONS = 4;
+constexpr int EW_MAX_REG = 8;   // wall regions of an embedded-wall launch (4 xy boxes x 2 z ranges)
 constexpr int SU = 9;           // u ring stages  (= 2R+1)
 constexpr int SP = 3;           // u_prev/vdt2 ring stages of the TB2 kernel (divides 9)
 #ifndef W25_PACKED
@@ -120,6 +124,23 @@ struct StreamParams {
   // stored eta through the u_prev/vdt2 ring (MODE_WALL_ETA): [nz][ny][pitch]
   // fp32, box (CW + 8) x (TY + 2), out-of-range cells (eta = 0) zero-filled
   alignas(64) CUtensorMap tm_eta;
+  // embedded walls (MODE_INNER_EW): the PML wall regions, cut into 16 x 8 tiles
+  // x z-chunks of cz planes ("units"), claimed by the CTAs' wall warps from a
+  // global ticket while their interior tile streams
+  struct Ew {
+    int nreg;                   // wall regions (same z-chunk count in each)
+    Region reg[EW_MAX_REG];     // ntx, nty in 16 x 8 tiles; blk0 = first tile of the region within a chunk
+    int cz, ntile, nunits;      // chunk length, tiles per chunk, units (ntile x chunks)
+    int min_rem;                // claim while the CTA's interior has >= min_rem planes to go
+    int last_blk;               // CTAs >= last_blk (the last wave) also claim once their interior is done
+    unsigned* ctr;              // [0] next unit, [1] CTAs whose wall warps have finished (self-resetting)
+    int pf;                     // L2 prefetch distance of the wall loads (planes beyond the ring; 0 = off)
+    unsigned long long* dbg;    // timing probe (WAVE25_EW_DBG): [0/1] ns, planes claimed during the
+                                // interior, [2/3] in the last wave's mop-up, [4/5] units
+    alignas(64) CUtensorMap tu; // u^n, box (16 + 2R) x (8 + 2R)
+    alignas(64) CUtensorMap tup;  // u^{n-1}, box 16 x 8
+    alignas(64) CUtensorMap tv;   // vdt2, box 16 x 8
+  } ew;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
@@ -150,7 +171,19 @@ template <> __device__ __forceinline__ const CoefT<double>& coef_of<double>(cons
 // that gives its registers back (setmaxnreg.dec to 24) so that the consumer
 // warpgroups can raise theirs to RA (setmaxnreg.inc) -- Blackwell/Hopper
 // warp-specialised register reallocation.  Needs NWC % 4 == 0.
-template <int TX, int CW, int TY, int TYT, int MINB = 2, int RA = 0, typename T = float, int ETA = 0>
+// embedded wall warps (MODE_INNER_EW): 16 x 8 tiles, two warps of 32 lanes x 2 points
+constexpr int EW_CW = 16, EW_TY = 8;
+constexpr int EW_SW = EW_CW + 2 * R;                 // u box row (floats)
+constexpr int EW_US = EW_SW * (EW_TY + 2 * R);       // u stage (floats)
+constexpr int EW_PS = EW_CW * EW_TY;                 // u_prev / vdt2 stage (floats)
+constexpr int EW_SPN = 3;                            // u_prev / vdt2 ring depth
+constexpr int EW_RP = 64;                            // producer-warpgroup registers (TMA warp + wall warps)
+constexpr int EW_RC = 104;                           // consumer registers (512 x 104 + 128 x 64 = 640 x 96)
+constexpr int EW_COEF = 64 * 8;                      // per wall lane: cg, A, B, rB of its 2 points (floats)
+constexpr int EW_BYTES_ = (SU * EW_US + 2 * EW_SPN * EW_PS + EW_COEF) * 4 + 2 * (SU + EW_SPN) * 8 + 16;
+constexpr int EW_BYTES = (EW_BYTES_ + 127) / 128 * 128;
+
+template <int TX, int CW, int TY, int TYT, int MINB = 2, int RA = 0, typename T = float, int ETA = 0, int EWB = 0>
 struct StreamCfg {
   static constexpr int NV = VecT<T>::N;                     // x points per lane vector
   static constexpr int LXW = (CW / NV) < 8 ? (CW / NV) : 8; // vector lanes per warp row
@@ -186,12 +219,14 @@ struct StreamCfg {
   // stages), so more of those two streams is in flight per SM
   static constexpr int fits_(int n) {
     return (SWZ_ ? 1024 : 0) + (SU * U_STAGE + 2 * n * P_STAGE) * (int)sizeof(T) + n * E_STAGE * 4 +
-               2 * (SU + n) * 8 + 4 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
+               2 * (SU + n) * 8 + (EWB ? EWB + 128 : 0) + 4 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
   }
   static constexpr int SPN = (W25_SP_MAX >= 5 && fits_(5)) ? 5 : (W25_SP_MAX >= 4 && fits_(4)) ? 4 : 3;
   static constexpr int E_OFF = (SU * U_STAGE + 2 * SPN * P_STAGE) * (int)sizeof(T);    // bytes (eta ring)
   static constexpr int BAR_OFF = E_OFF + SPN * E_STAGE * 4;                             // bytes
-  static constexpr int TAB_OFF = BAR_OFF + 2 * (SU + SPN) * 8;
+  // embedded wall warps' region (128-B aligned TMA stages), then the PML tables
+  static constexpr int EW_OFF = (BAR_OFF + 2 * (SU + SPN) * 8 + 127) / 128 * 128;
+  static constexpr int TAB_OFF = EWB ? EW_OFF + EWB : BAR_OFF + 2 * (SU + SPN) * 8;
   // u boxes whose rows are exactly one 128-B line (the fp32 x walls, 24 + 8
   // floats) are loaded with the TMA 128-B swizzle: a float4 column read across
   // the 8 rows of a warp would otherwise hit the same 16 banks (2 wavefronts
@@ -244,6 +279,23 @@ __device__ __noinline__ typename VecT<T>::V cap_update(typename VecT<T>::V L, ty
 // (w+2)-entry table (eta_{w+1} = 0 outside), the grad-eta . grad-u term and
 // the damped update; points with d = 0 take the inner formula (identical
 // arithmetic to the naive kernel).  Used for wall planes in / next to a cap.
+// one point of the general PML path: distances dx(-1, 0, +1) along x, dy, dz
+// (and their +-1 neighbours), eta on the 7-point star from the table
+template <typename T>
+__device__ __forceinline__ T pml_point(T Lc, T uc, T upc, T vc, T xp, T xm, T yp, T ym, T zp, T zm, int dxm,
+                                       int dx, int dxp, int dy, int dym, int dyp, int dz, int dzm, int dzp,
+                                       const PmlGeoT<T>& G, const T* stab, bool fast) {
+  const int dxy = max(dx, dy);
+  const int d = max(dxy, dz);
+  if (d == 0) return upd_inner(Lc, uc, upc, vc);
+  const T exp_ = stab[max(max(dxp, dy), dz)], exm = stab[max(max(dxm, dy), dz)];
+  const T eyp = stab[max(max(dx, dyp), dz)], eym = stab[max(max(dx, dym), dz)];
+  const T ezp = stab[max(dxy, dzp)], ezm = stab[max(dxy, dzm)];
+  const T g = add_rn(add_rn(gterm(exp_, exm, xp, xm, G.i2hx), gterm(eyp, eym, yp, ym, G.i2hy)),
+                     gterm(ezp, ezm, zp, zm, G.i2hz));
+  return upd_pml_t(Lc, g, uc, upc, vc, stab[G.TN + d], stab[2 * G.TN + d], stab[3 * G.TN + d], fast);
+}
+
 template <typename T>
 __device__ __noinline__ typename VecT<T>::V pml_row_call(typename VecT<T>::V L, typename VecT<T>::V C,
                                                          typename VecT<T>::V up, typename VecT<T>::V v,
@@ -259,24 +311,10 @@ __device__ __noinline__ typename VecT<T>::V pml_row_call(typename VecT<T>::V L, 
   for (int c = 0; c < NV + 2; ++c) dxs[c] = dist1(gx - 1 + c, G.nx, G.w);
   T res[NV];
 #pragma unroll
-  for (int c = 0; c < NV; ++c) {
-    const int dx = dxs[c + 1];
-    const int dxy = max(dx, dy);
-    const int d = max(dxy, dz);
-    const T uc = vget(C, c), upc = vget(up, c), vc = vget(v, c);
-    const T Lc = vget(L, c);
-    if (d == 0) {
-      res[c] = upd_inner(Lc, uc, upc, vc);
-    } else {
-      const T exp_ = stab[max(max(dxs[c + 2], dy), dz)], exm = stab[max(max(dxs[c], dy), dz)];
-      const T eyp = stab[max(max(dx, dyp), dz)], eym = stab[max(max(dx, dym), dz)];
-      const T ezp = stab[max(dxy, dzp)], ezm = stab[max(dxy, dzm)];
-      const T g = add_rn(add_rn(gterm(exp_, exm, vget(xp, c), vget(xm, c), G.i2hx),
-                                gterm(eyp, eym, vget(yp, c), vget(ym, c), G.i2hy)),
-                         gterm(ezp, ezm, vget(zp, c), vget(zm, c), G.i2hz));
-      res[c] = upd_pml_t(Lc, g, uc, upc, vc, stab[G.TN + d], stab[2 * G.TN + d], stab[3 * G.TN + d], fast);
-    }
-  }
+  for (int c = 0; c < NV; ++c)
+    res[c] = pml_point<T>(vget(L, c), vget(C, c), vget(up, c), vget(v, c), vget(xp, c), vget(xm, c), vget(yp, c),
+                          vget(ym, c), vget(zp, c), vget(zm, c), dxs[c], dxs[c + 1], dxs[c + 2], dy, dym, dyp, dz,
+                          dzm, dzp, G, stab, fast);
   return vmake<T>(res);
 }
 
@@ -313,6 +351,283 @@ __device__ __forceinline__ typename VecT<T>::V pml_row_eta_s(
   return vmake<T>(res);
 }
 
+// ---------------------------------------------------------------------------
+// Embedded wall warps (MODE_INNER_EW).  Two warps of the
+// interior CTA's producer warpgroup compute the PML walls while the consumer
+// warps stream the interior tile: the walls then cost SM issue slots the
+// memory-bound interior leaves idle instead of whole SMs of their own.  Work
+// unit = one 16 x 8 wall tile x one z-chunk, claimed from a global ticket;
+// lane (warp k, lane l) owns row 4k + l/8, x points 2 (l % 8) + {0, 1}.
+// Own small TMA ring (9 u stages of 24 x 16, 3 u_prev/vdt2 stages of 16 x 8),
+// filled by lane 0 of wall warp 0; the register queue shifts (one plane per
+// iteration, compact code: the interior's hot loop keeps the I-cache).
+// Arithmetic per point is exactly the wall kernels' (column-constant /
+// row-uniform fast paths on z-interior planes, pml_point elsewhere), so the
+// result is bitwise the separate-launch one.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 lds2(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ void st_cs_f2(float* p, float2 v) {
+  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ float f2get(const float2& v, int c) { return c == 0 ? v.x : v.y; }
+__device__ __forceinline__ void bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void ew_body(const StreamParams& P, unsigned char* ewb, const float* stab, int int_planes,
+                                        int wk, int lane) {
+  const StreamParams::Ew& E = P.ew;
+  float* su = reinterpret_cast<float*>(ewb);
+  float* sp = su + SU * EW_US;                              // [EW_SPN][u_prev | vdt2][EW_PS]
+  float* sco = sp + EW_SPN * 2 * EW_PS;                      // [64 lanes][cg0, cg1, A0, A1, B0, B1, rB0, rB1]
+  uint64_t* full_u = reinterpret_cast<uint64_t*>(sco + EW_COEF);
+  uint64_t* empty_u = full_u + SU;
+  uint64_t* full_p = empty_u + SU;
+  uint64_t* empty_p = full_p + EW_SPN;
+  volatile int* s_ew = reinterpret_cast<volatile int*>(empty_p + EW_SPN);   // [0] interior planes done, [1] unit
+  const Coef& K = P.k;
+  const int TABN = P.w + 2;
+  const bool prod = wk == 0 && lane == 0;
+  const int r = wk * 4 + (lane >> 3), c2 = lane & 7;
+  float* myco = sco + (wk * 32 + lane) * 8;
+  PmlGeoT<float> PG;
+  PG.nx = P.nx; PG.ny = P.ny; PG.nzg = P.nzg; PG.w = P.w; PG.TN = TABN;
+  PG.i2hx = K.i2h[0]; PG.i2hy = K.i2h[1]; PG.i2hz = K.i2h[2];
+  const uint64_t pol_u = policy_evict_normal(), pol_s = policy_evict_first();
+  uint32_t useq = 0, pseq = 0;                              // ring sequence numbers (persist across units)
+  int cx0 = 0, ty0 = 0;
+  // u plane `pl` -> ring load `n` (stage n % 9); the stage's previous use (n - 9) must be released by both warps
+  auto issue_u = [&](uint32_t n, int pl) {
+    const int st = (int)(n % SU);
+    if (n >= (uint32_t)SU) {
+      mbar_wait(&empty_u[st], ((n / SU) - 1) & 1);
+      fence_proxy_async_smem();
+    }
+    mbar_arrive_expect_tx(&full_u[st], EW_US * 4);
+    tma_load_3d(su + st * EW_US, &E.tu, &full_u[st], cx0 - R, ty0 - R, pl + R, pol_u);
+    if (E.pf > 0) tma_prefetch_3d(&E.tu, cx0 - R, ty0 - R, pl + E.pf + R);
+  };
+  auto issue_p = [&](uint32_t n, int pl) {
+    const int st = (int)(n % EW_SPN);
+    if (n >= (uint32_t)EW_SPN) {
+      mbar_wait(&empty_p[st], ((n / EW_SPN) - 1) & 1);
+      fence_proxy_async_smem();
+    }
+    mbar_arrive_expect_tx(&full_p[st], 2 * EW_PS * 4);
+    tma_load_3d(sp + st * 2 * EW_PS, &E.tup, &full_p[st], cx0, ty0, pl + R, pol_s);
+    tma_load_3d(sp + st * 2 * EW_PS + EW_PS, &E.tv, &full_p[st], cx0, ty0, pl, pol_s);
+    if (E.pf > 0) {
+      tma_prefetch_3d(&E.tup, cx0, ty0, pl + E.pf + R);
+      tma_prefetch_3d(&E.tv, cx0, ty0, pl + E.pf);
+    }
+  };
+
+#pragma unroll 1
+  while (true) {
+    // ---- claim a unit (lane 0 of wall warp 0), pacing on the interior ----
+    if (prod) {
+      int u = -1;
+#pragma unroll 1
+      while (true) {
+        const int rem = int_planes - s_ew[0];
+        const bool last = (int)blockIdx.x >= E.last_blk;
+        if (rem >= E.min_rem || (last && rem <= 0)) {
+          const unsigned t = atomicAdd(E.ctr, 1u);
+          u = t < (unsigned)E.nunits ? (int)t : -1;
+          break;
+        }
+        if (!last) break;                                   // not the last wave: leave the rest to others
+        __nanosleep(256);                                   // last wave: claim again once the interior is done
+      }
+      s_ew[1] = u;
+    }
+    bar_sync_n(2, 64);
+    const int u = s_ew[1];
+    bar_sync_n(3, 64);                                      // (s_ew[1] read by both before it is rewritten)
+    if (u < 0) break;
+    unsigned long long t_unit = 0;
+    const bool mop = s_ew[0] >= int_planes;
+    if (E.dbg && prod) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_unit));
+    const int k = u / E.ntile;
+    const int t = u - k * E.ntile;
+    int ri = 0;
+#pragma unroll 1
+    while (ri + 1 < E.nreg && t >= E.reg[ri + 1].blk0) ++ri;
+    const Region& g = E.reg[ri];
+    const int lt = t - g.blk0;
+    const int tyi = lt / g.ntx, txi = lt - tyi * g.ntx;
+    cx0 = g.ax0 + txi * EW_CW;
+    ty0 = g.y0 + tyi * EW_TY;
+    const int zs = g.z0 + k * E.cz, ze = min(zs + E.cz, g.z1);
+    const int np = ze - zs, nu = np + 2 * R;
+    if (prod) {
+      for (int j = 0; j < SU && j < nu; ++j) issue_u(useq + j, zs - R + j);
+      for (int j = 0; j < EW_SPN && j < np; ++j) issue_p(pseq + j, zs + j);
+    }
+    // ---- per-lane geometry, PML coefficients -----------------------------
+    const int gx = cx0 + 2 * c2, gy = ty0 + r;
+    unsigned mask = 0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      if (gx + c >= g.x0 && gx + c < g.x1 && gy >= g.y0 && gy < g.y1) mask |= 1u << c;
+    bool all_dx0 = true, all_dy0 = true;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+      if ((mask >> c) & 1u) {
+        all_dx0 &= dist1(gx + c, P.nx, P.w) == 0;
+        all_dy0 &= dist1(gy, P.ny, P.w) == 0;
+      }
+    all_dx0 = __all_sync(0xffffffffu, all_dx0);
+    all_dy0 = __all_sync(0xffffffffu, all_dy0);
+    const int wkind = all_dx0 ? 1 : (all_dy0 ? 2 : 0);     // 1: y-wall rows, 2: x-wall columns, 0: general
+    {
+      const int dy = dist1(gy, P.ny, P.w);
+      const float cgy = dy == 0 ? 0.f
+                                : mul_rn(sub_rn(stab[dist1(gy + 1, P.ny, P.w)], stab[dist1(gy - 1, P.ny, P.w)]),
+                                         K.i2h[1]);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int dx = dist1(gx + c, P.nx, P.w);
+        const float cgx = dx == 0 ? 0.f
+                                  : mul_rn(sub_rn(stab[dist1(gx + c + 1, P.nx, P.w)], stab[dist1(gx + c - 1, P.nx, P.w)]),
+                                           K.i2h[0]);
+        const int d = wkind == 1 ? dy : dx;
+        myco[c] = wkind == 1 ? cgy : cgx;
+        myco[2 + c] = stab[TABN + d];
+        myco[4 + c] = stab[2 * TABN + d];
+        myco[6 + c] = stab[3 * TABN + d];
+      }
+    }
+    // ---- warm-up: planes zs-4 .. zs+3 -> queue ------------------------------
+    const int own = (r + R) * EW_SW + R + 2 * c2;          // my centre in a u stage
+    float2 q[2 * R + 1];
+#pragma unroll
+    for (int j = 0; j < 2 * R; ++j) {
+      const uint32_t n = useq + j;
+      mbar_wait(&full_u[n % SU], (n / SU) & 1);
+      q[j] = lds2(su + (n % SU) * EW_US + own);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j < R; ++j) {                           // planes zs-4..zs-1: only their own rows were needed
+      if (lane == 0) mbar_arrive(&empty_u[(useq + j) % SU]);
+      if (prod && j + SU < nu) issue_u(useq + j + SU, zs - R + j + SU);
+    }
+    float* optr = static_cast<float*>(P.out) + (int64_t)(zs + R) * P.plane + (int64_t)gy * P.pitch + gx;
+    const bool fast = P.fastdiv != 0;
+    // ---- planes -------------------------------------------------------------
+#pragma unroll 1
+    for (int i = 0; i < np; ++i) {
+      const int z = zs + i;
+      {
+        const uint32_t n = useq + i + 2 * R;                // leading plane z + 4
+        mbar_wait(&full_u[n % SU], (n / SU) & 1);
+        q[2 * R] = lds2(su + (n % SU) * EW_US + own);
+      }
+      const int sc = (int)((useq + i + R) % SU);            // centre plane z
+      const float* S = su + sc * EW_US + own;
+      float2 Y[2 * R + 1];
+#pragma unroll
+      for (int jj = 0; jj <= 2 * R; ++jj) Y[jj] = jj == R ? q[R] : lds2(S + (jj - R) * EW_SW);
+      const float2 xl0 = lds2(S - 4), xl1 = lds2(S - 2), xr0 = lds2(S + 2), xr1 = lds2(S + 4);
+      const float Xv[10] = {xl0.x, xl0.y, xl1.x, xl1.y, q[R].x, q[R].y, xr0.x, xr0.y, xr1.x, xr1.y};
+      const uint32_t pn = pseq + i;
+      const int spp = (int)(pn % EW_SPN);
+      mbar_wait(&full_p[spp], (pn / EW_SPN) & 1);
+      const float2 upv = lds2(sp + spp * 2 * EW_PS + r * EW_CW + 2 * c2);
+      const float2 vv = lds2(sp + spp * 2 * EW_PS + EW_PS + r * EW_CW + 2 * c2);
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty_u[sc]);
+        mbar_arrive(&empty_p[spp]);
+      }
+      if (prod) {
+        if (i + R + SU < nu) issue_u(useq + i + R + SU, z + SU);
+        if (i + EW_SPN < np) issue_p(pn + EW_SPN, z + EW_SPN);
+      }
+      float L[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        L[c] = mul_rn(K.c0, Xv[4 + c]);
+#pragma unroll
+        for (int m = 1; m <= R; ++m) L[c] = fma_rn(K.cx[m - 1], add_rn(Xv[4 + c + m], Xv[4 + c - m]), L[c]);
+#pragma unroll
+        for (int m = 1; m <= R; ++m) L[c] = fma_rn(K.cy[m - 1], add_rn(f2get(Y[R + m], c), f2get(Y[R - m], c)), L[c]);
+#pragma unroll
+        for (int m = 1; m <= R; ++m) L[c] = fma_rn(K.cz[m - 1], add_rn(f2get(q[R + m], c), f2get(q[R - m], c)), L[c]);
+      }
+      const int kg = z + P.zoff;
+      float o[2];
+      if (wkind != 0 && kg > P.w && kg < P.nzg - P.w - 1) {
+        const float4 c0 = *reinterpret_cast<const float4*>(myco), c1 = *reinterpret_cast<const float4*>(myco + 4);
+        const float cg[2] = {c0.x, c0.y}, A[2] = {c0.z, c0.w};
+        float num[2];
+        const float Bd[2] = {c1.x, c1.y}, rBd[2] = {c1.z, c1.w};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float gd = wkind == 2 ? mul_rn(cg[c], mul_rn(sub_rn(Xv[5 + c], Xv[3 + c]), K.i2h[0]))
+                                      : mul_rn(cg[c], mul_rn(sub_rn(f2get(Y[R + 1], c), f2get(Y[R - 1], c)), K.i2h[1]));
+          num[c] = pml_num(L[c], gd, Xv[4 + c], f2get(upv, c), f2get(vv, c), A[c]);
+        }
+        div_table_row<float, 2>(num, Bd, rBd, fast, o);
+      } else {
+        const int dy = dist1(gy, P.ny, P.w), dym = dist1(gy - 1, P.ny, P.w), dyp = dist1(gy + 1, P.ny, P.w);
+        const int dz = dist1(kg, P.nzg, P.w), dzm = dist1(kg - 1, P.nzg, P.w), dzp = dist1(kg + 1, P.nzg, P.w);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          o[c] = pml_point<float>(L[c], Xv[4 + c], f2get(upv, c), f2get(vv, c), Xv[5 + c], Xv[3 + c],
+                                  f2get(Y[R + 1], c), f2get(Y[R - 1], c), f2get(q[R + 1], c), f2get(q[R - 1], c),
+                                  dist1(gx + c - 1, P.nx, P.w), dist1(gx + c, P.nx, P.w),
+                                  dist1(gx + c + 1, P.nx, P.w), dy, dym, dyp, dz, dzm, dzp, PG, stab, fast);
+      }
+      if (mask == 3u) {
+        st_cs_f2(optr, make_float2(o[0], o[1]));
+      } else {
+        if (mask & 1u) optr[0] = o[0];
+        if (mask & 2u) optr[1] = o[1];
+      }
+      // fused halo exchange of edge planes (both targets independent, as in stream_body)
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        float* rbase = nullptr;
+        if (side == 0 && z < R && P.rlo) rbase = static_cast<float*>(P.rlo) + (int64_t)z * P.plane;
+        if (side == 1 && z >= P.nzl - R && P.rhi) rbase = static_cast<float*>(P.rhi) + (int64_t)(z - (P.nzl - R)) * P.plane;
+        if (rbase) {
+          float* rp = rbase + (int64_t)gy * P.pitch + gx;
+          if (mask & 1u) rp[0] = o[0];
+          if (mask & 2u) rp[1] = o[1];
+        }
+      }
+      optr += P.plane;
+#pragma unroll
+      for (int j = 0; j < 2 * R; ++j) q[j] = q[j + 1];
+    }
+    // the last 4 loads (planes ze..ze+3) were only ever leading planes: release
+    // them so the ring can be refilled for the next unit
+    __syncwarp();
+    if (lane == 0)
+      for (int j = np + R; j < nu; ++j) mbar_arrive(&empty_u[(useq + j) % SU]);
+    useq += nu;
+    pseq += np;
+    if (E.dbg && prod) {
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      atomicAdd(E.dbg + (mop ? 2 : 0), t1 - t_unit);
+      atomicAdd(E.dbg + (mop ? 3 : 1), (unsigned long long)np);
+      atomicAdd(E.dbg + (mop ? 5 : 4), 1ull);
+    }
+  }
+  // every CTA's wall warps finish exactly once; the last one re-arms the ticket
+  // for the next launch (no claim can follow: all CTAs have made their last)
+  if (prod) {
+    __threadfence();
+    if (atomicAdd(E.ctr + 1, 1u) == gridDim.x - 1) {
+      atomicExch(E.ctr, 0u);
+      atomicExch(E.ctr + 1, 0u);
+    }
+  }
+}
+
 // The body of one work unit (tile x z-chunk) of k_stream; `unit0` = its index
 // in the launch's region list (blockIdx.x for k_stream, remapped by k_mix).
 // CL > 1 (interior only, TY = 2R): CL CTAs of a thread-block cluster hold CL
@@ -333,7 +648,12 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
             const CUtensorMap& tm_up,   // u^{n-1}, box (CW, TY, 1)
             const CUtensorMap& tm_v,    // vdt2, box (CW, TY, 1)
             const StreamParams& P, const int unit0) {
-  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T, MODE == MODE_WALL_ETA>;
+  constexpr bool EW = MODE == MODE_INNER_EW;               // embedded wall warps
+  constexpr bool INN = MODE == MODE_INNER || EW;             // interior update in the consumer warps
+  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T, MODE == MODE_WALL_ETA, EW ? EW_BYTES : 0>;
+  static_assert(!EW || (sizeof(T) == 4 && RA == EW_RC && PAIR == 0 && CL == 1 && C::NWC % 4 == 0 &&
+                        C::NWC / 4 * EW_RC + EW_RP <= (C::NWC / 4 + 1) * C::MAXR),
+                "embedded walls: fp32 interior with a producer warpgroup of 4 warps (TMA + 2 wall warps + 1)");
   using V = typename VecT<T>::V;
   constexpr int NV = C::NV;
   static_assert(CL == 1 || (MODE == MODE_INNER && C::NH == 1 && TY == 2 * R && TYT == 1 && PAIR == 0 && CL <= 8),
@@ -439,6 +759,17 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
     for (int s = 0; s < SU; ++s) { mbar_init(&full_u[s], 1); mbar_init(&empty_u[s], C::NWC * (crank > 0 ? 2 : 1)); }
 #pragma unroll
     for (int s = 0; s < C::SPN; ++s) { mbar_init(&full_p[s], 1); mbar_init(&empty_p[s], C::NWC); }
+    if (EW) {
+      uint64_t* eb = reinterpret_cast<uint64_t*>(smem_raw + C::EW_OFF + (SU * EW_US + 2 * EW_SPN * EW_PS + EW_COEF) * 4);
+      for (int s = 0; s < SU; ++s) { mbar_init(&eb[s], 1); mbar_init(&eb[SU + s], 2); }
+      for (int s = 0; s < EW_SPN; ++s) { mbar_init(&eb[2 * SU + s], 1); mbar_init(&eb[2 * SU + EW_SPN + s], 2); }
+      int* sew = reinterpret_cast<int*>(eb + 2 * (SU + EW_SPN));
+      sew[0] = 0;
+      sew[1] = -1;
+      prefetch_tmap(&P.ew.tu);
+      prefetch_tmap(&P.ew.tup);
+      prefetch_tmap(&P.ew.tv);
+    }
     fence_mbar_init();
   }
   for (int i = tid; i < 4 * TABN; i += C::NT) stab[i] = static_cast<const T*>(P.tab)[i];
@@ -450,7 +781,13 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
   if (wid >= C::NWC) {
     // the cluster producer (multicast masks, remote barriers) needs 32 registers;
     // the budget 4 x 112 + 32 = 5 x 96 still holds for the interior tile
-    if (RA > 0 && CL > 1) {
+    if (EW) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(EW_RP) : "memory");
+      if (wid == C::NWC + 1 || wid == C::NWC + 2) {       // the wall warps
+        ew_body(P, smem_raw + C::EW_OFF, reinterpret_cast<const float*>(stab), ze - zs, wid - C::NWC - 1, lane);
+        return;
+      }
+    } else if (RA > 0 && CL > 1) {
       static_assert(CL == 1 || C::NWC / 4 * RA + 32 <= (C::NWC / 4 + 1) * C::MAXR, "cluster producer registers");
       asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
     } else if (RA > 0) {
@@ -861,7 +1198,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       T L[TYT][NV];
       // fp32: the 25-point sum on packed pairs of x-points (FMUL2/FADD2/FFMA2,
       // bitwise the scalar chain below element by element, half the issue slots)
-      constexpr bool PK = sizeof(T) == 4 && W25_PACKED && MODE == MODE_INNER;   // (walls: scalar, no spills)
+      constexpr bool PK = sizeof(T) == 4 && W25_PACKED && INN;   // (walls: scalar, no spills)
       if (PK && MODE != MODE_NULL) {
         f2_t L2[TYT][2];
         auto pr = [&](const V& v, int h) -> f2_t {
@@ -1008,7 +1345,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
           for (int c = 0; c < NV; ++c) o[c] = vget(upv[r], c) + vget(vv[r], c) + (c == 0 ? L[r][0] : T(0));
           res[r] = vmake<T>(o);
         }
-      } else if (MODE == MODE_INNER || (MODE == MODE_FUSED && !warp_xy_pml)) {
+      } else if (INN || (MODE == MODE_FUSED && !warp_xy_pml)) {
         if (kg >= P.w && kg < P.nzg - P.w) {
 #pragma unroll
           for (int r = 0; r < TYT; ++r) {
@@ -1184,6 +1521,10 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
         }
       }
       optr += P.plane;
+      // embedded walls: the interior's progress paces the wall warps' claims
+      if (EW && tid == 0)
+        *reinterpret_cast<volatile int*>(smem_raw + C::EW_OFF + (SU * EW_US + 2 * EW_SPN * EW_PS + EW_COEF) * 4 +
+                                         2 * (SU + EW_SPN) * 8) = z + 1 - zs;
     }
   }
   if (CL > 1) cluster_sync_all();           // the next CTA's consumers may still arrive on our barriers

@@ -70,7 +70,7 @@ struct KInfo {
 template <int TX, int CW, int TY, int TYT, int MODE, int MINB = 2, int RA = 0, typename T = float, int PAIR = 0,
           int CL = 1>
 static KInfo kinfo(const char* name) {
-  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T, MODE == MODE_WALL_ETA>;
+  using C = StreamCfg<TX, CW, TY, TYT, MINB, RA, T, MODE == MODE_WALL_ETA, MODE == MODE_INNER_EW ? EW_BYTES : 0>;
   // tx = width of the u TMA box minus its halo (the half width for split boxes)
   return KInfo{(void*)k_stream<TX, CW, TY, TYT, MODE, MINB, RA, T, PAIR, CL>, C::HW, CW, TY, C::NT, &C::smem_bytes,
                name, CL, C::SWZ};
@@ -93,6 +93,11 @@ static const KInfo* inner_variants(int* n) {
       kinfo<240, 240, 8, 1, MODE_INNER, 1, 112>("240x8x1r"),
       kinfo<256, 256, 8, 1, MODE_INNER, 1, 112>("256x8x1r"),
       kinfo<248, 248, 8, 2, MODE_INNER, 1>("248x8x2"),
+      // two rows per thread (y-neighbour LDS per row 8 -> 4: the interior is
+      // close to shared-memory-bound, ncu l1tex 78 %): 8 consumer warps at 232
+      // registers + the producer warpgroup at 24
+      kinfo<248, 248, 8, 2, MODE_INNER, 1, 232>("248x8x2r"),
+      kinfo<248, 248, 8, 1, MODE_INNER, 1, 104>("248x8x1r104"),   // consumers at 104 registers (A/B)
       kinfo<248, 248, 4, 1, MODE_INNER, 1>("248x4x1"),
       kinfo<248, 248, 8, 2, MODE_NULL, 1>("null248x8x2"),
       kinfo<224, 224, 4, 1, MODE_INNER, 1>("224x4x1"),
@@ -153,8 +158,10 @@ static KInfo pick(const KInfo* v, int n, const char* env) {
 // KI_WALLX_E / KI_WALLY_E: the wall kernels of the stored-eta mode
 // KI_PAIR: the two-step-through-L2 interior kernel
 // KI_SEAM: both x walls as seams (MODE_SEAM)
+// KI_EW: the interior kernel with embedded wall warps (MODE_INNER_EW)
+// KI_EWALL: not launched -- the TMA maps (16 x 8 boxes) of KI_EW's wall warps
 enum { KI_INNER = 0, KI_WALLX = 1, KI_WALLY = 2, KI_FUSED = 3, KI_WALLX_E = 4, KI_WALLY_E = 5, KI_PAIR = 6,
-       KI_SEAM = 7, KI_N = 8 };
+       KI_SEAM = 7, KI_EW = 8, KI_EWALL = 9, KI_N = 10 };
 static bool is_wall(int ki) {
   return ki == KI_WALLX || ki == KI_WALLY || ki == KI_WALLX_E || ki == KI_WALLY_E || ki == KI_SEAM;
 }
@@ -201,6 +208,13 @@ static void init_kernels() {
     g_k[0][KI_SEAM] = pick(sv, 2, "WAVE25_SEAM_TILE");
   }
   g_k[1][KI_SEAM] = g_k[1][KI_WALLX];   // (fp32 only; fp64 plans never build seam launches)
+  g_k[0][KI_EW] = kinfo<248, 248, 8, 1, MODE_INNER_EW, 1, EW_RC>("ew248x8x1r");
+  {
+    KInfo m = g_k[0][KI_EW];                 // (same function and smem size: the attribute loops stay consistent)
+    m.tx = EW_CW; m.cw = EW_CW; m.ty = EW_TY; m.swz = false; m.name = "ewall16x8";
+    g_k[0][KI_EWALL] = m;
+  }
+  g_k[1][KI_EW] = g_k[1][KI_EWALL] = g_k[1][KI_INNER];   // (fp32 only)
   done = true;
 }
 #define KTX(ki) (g_k[P->prec][ki].tx)
@@ -283,7 +297,7 @@ struct wave_plan {
   Stats* stats_d = nullptr;
   // launch plans
   Maps maps[KI_N];
-  int occ[KI_N] = {1, 1, 1, 1, 1, 1, 1, 1};
+  int occ[KI_N] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
   bool fused = false;                // WAVE25_FUSED=1: one launch, per-warp paths (measured slower)
   int pf = 1;                        // L2 prefetch distance (WAVE25_PF), measured best
   int wall_pf = -1;                  // wall kernels' L2 prefetch distance (WAVE25_WALL_PF; -1 = pf)
@@ -344,6 +358,13 @@ struct wave_plan {
   double peer_timeout_s = 300.0;           // k_peer_wait bound (WAVE25_PEER_TIMEOUT_S / wave_set_peer_timeout)
   bool remote = false;                     // enqueue with remote edge stores
   cudaGraphExec_t gexec_peer[2] = {nullptr, nullptr};
+  // embedded wall warps (MODE_INNER_EW)
+  bool ew_on = false;                      // WAVE25_EW=1
+  int ew_cz = 0;                           // WAVE25_EW_CZ: wall unit length in planes (0 = auto)
+  int ew_rem = -1;                         // WAVE25_EW_REM: claim while >= this many interior planes remain (-1 = cz)
+  unsigned* ew_ctr = nullptr;              // [3 launch sets][2] tickets (self-resetting)
+  int ew_pf = 8;                           // WAVE25_EW_PF: L2 prefetch distance of the wall loads
+  unsigned long long* ew_dbg = nullptr;    // WAVE25_EW_DBG=1: wall-unit timing probe (6 counters)
 };
 
 // element-offset pointer into a buffer of the plan's precision
@@ -582,6 +603,56 @@ static bool seam_active(const wave_plan* P) {
          P->d.kernel == WAVE_KERNEL_STREAM;
 }
 
+static const char* ablation_shape();
+
+// embedded wall warps: fp32 default-path plans with PML walls only (any mode
+// that shapes the interior or the walls differently keeps separate launches)
+static bool ew_wanted(const wave_plan* P) {
+  const int nx = (int)P->d.nx, ny = (int)P->d.ny, w = P->d.pml_width;
+  return P->ew_on && P->prec == 0 && w > 0 && nx > 2 * w && ny > 2 * w && !P->eta_on && !P->fused && !P->xfuse &&
+         P->xwall_extra == 0 && !seam_active(P) && P->mix == 0 && P->d.kernel == WAVE_KERNEL_STREAM &&
+         !ablation_shape() && !getenv("WAVE25_INNER_TILE");
+}
+
+// the wall regions of an embedded-wall launch over the z ranges `zr`: x walls
+// over the full y range (corners included), y walls over the inner x range,
+// 16 x 8 tiles, z-chunks of ew_cz planes, units chunk-major
+static bool attach_walls(wave_plan* P, Launch* L, const std::vector<ZRange>& zr, int set) {
+  const int nx = (int)P->d.nx, ny = (int)P->d.ny, w = P->d.pml_width;
+  StreamParams::Ew& E = L->p.ew;
+  int nzmax = 0;
+  for (const ZRange& z : zr) nzmax = std::max(nzmax, z.z1 - z.z0);
+  const int cz = std::max(1, std::min(nzmax, P->ew_cz > 0 ? P->ew_cz : std::max(8, L->p.cz / 3)));
+  const std::array<int, 4> xy[4] = {{0, w, 0, ny}, {nx - w, nx, 0, ny}, {w, nx - w, 0, w}, {w, nx - w, ny - w, ny}};
+  E.nreg = 0;
+  int tiles = 0, nzc = -1;
+  for (const ZRange& z : zr)
+    for (const auto& b : xy) {
+      if (b[1] <= b[0] || b[3] <= b[2] || z.z1 <= z.z0) continue;
+      if (E.nreg == EW_MAX_REG) return false;
+      Region& g = E.reg[E.nreg++];
+      g.x0 = b[0]; g.x1 = b[1]; g.y0 = b[2]; g.y1 = b[3]; g.z0 = z.z0; g.z1 = z.z1;
+      g.ax0 = b[0] & ~3;
+      g.ntx = (b[1] - g.ax0 + EW_CW - 1) / EW_CW;
+      g.nty = (b[3] - b[2] + EW_TY - 1) / EW_TY;
+      g.nzc = (z.z1 - z.z0 + cz - 1) / cz;
+      if (nzc >= 0 && g.nzc != nzc) return false;           // (one chunk count per launch)
+      nzc = g.nzc;
+      g.blk0 = tiles;
+      tiles += g.ntx * g.nty;
+    }
+  if (E.nreg == 0) return false;
+  E.cz = cz;
+  E.ntile = tiles;
+  E.nunits = tiles * nzc;
+  E.min_rem = P->ew_rem >= 0 ? P->ew_rem : cz;
+  E.last_blk = std::max(0, L->nblk - P->occ[KI_EW] * P->nsm);
+  E.ctr = P->ew_ctr + 2 * set;
+  E.pf = P->ew_pf;
+  E.dbg = P->ew_dbg;
+  return true;
+}
+
 static wave_status build_launches(wave_plan* P) {
   const int nx = (int)P->d.nx, ny = (int)P->d.ny, nz = (int)P->d.nz, w = P->d.pml_width;
   std::vector<ZRange> all = {{0, nz}}, edges, inter;
@@ -606,6 +677,16 @@ static wave_status build_launches(wave_plan* P) {
       add_regions(P, KI_FUSED, {{0, nx, w, ny - w}}, *sets[s], &P->launches[s]);
       if (w > 0) add_regions(P, KI_WALLY, {{0, nx, 0, w}, {0, nx, ny - w, ny}}, *sets[s], &P->launches[s]);
       continue;
+    }
+    // embedded walls: one launch, the interior tiles' CTAs
+    // compute the four PML walls in their spare warps
+    if (ew_wanted(P)) {
+      std::vector<Launch> tmp;
+      add_regions(P, KI_EW, {{w, nx - w, w, ny - w}}, *sets[s], &tmp);
+      if (tmp.size() == 1 && attach_walls(P, &tmp[0], *sets[s], s)) {
+        P->launches[s].push_back(tmp[0]);
+        continue;
+      }
     }
     // interior kernel: inner xy footprint, all z (z caps plane-uniform); with a
     // stored eta the caps are not plane-uniform and go to the wall kernel
@@ -914,6 +995,11 @@ static wave_status launch_stream(wave_plan* P, const Launch& Lc, int ui, int upi
     const int64_t plane = P->L.pitch_x * P->d.ny;
     if (P->peers.lo_buf[upi]) p.rlo = eo(P, P->peers.lo_buf[upi], (P->peers.lo_nz + R) * plane);
     if (P->peers.hi_buf[upi]) p.rhi = P->peers.hi_buf[upi];
+  }
+  if (Lc.ki == KI_EW) {
+    p.ew.tu = P->maps[KI_EWALL].u[ui];
+    p.ew.tup = P->maps[KI_EWALL].up[upi];
+    p.ew.tv = P->maps[KI_EWALL].v;
   }
   const dim3 grid(Lc.nblk), block(kernel_threads(P, Lc.ki));
   const size_t smem = kernel_smem(P, Lc.ki);
@@ -1457,6 +1543,14 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_ORDER")) P->order = atoi(e);
   if (const char* e = getenv("WAVE25_FUSED")) P->fused = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_UPOL")) P->upol = atoi(e);
+  if (const char* e = getenv("WAVE25_EW")) P->ew_on = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_EW_CZ")) P->ew_cz = std::max(1, atoi(e));
+  if (const char* e = getenv("WAVE25_EW_REM")) P->ew_rem = atoi(e);
+  if (const char* e = getenv("WAVE25_EW_PF")) P->ew_pf = std::max(0, atoi(e));
+  if (getenv("WAVE25_EW_DBG") && atoi(getenv("WAVE25_EW_DBG")) != 0) {
+    cudaMalloc(&P->ew_dbg, 6 * sizeof(unsigned long long));
+    cudaMemset(P->ew_dbg, 0, 6 * sizeof(unsigned long long));
+  }
   cudaDeviceGetStreamPriorityRange(&P->prio_lo, &P->prio_hi);
   if (const char* e = getenv("WAVE25_L2MB")) P->l2_persist_mb = atoi(e);
   if (const char* e = getenv("WAVE25_L2HR")) P->l2_hit_ratio = (float)atof(e);
@@ -1473,7 +1567,9 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   const int T = P->d.pml_width + 2;
   if ((e = cudaMalloc(&P->tab_d, 4 * T * P->esz)) != cudaSuccess ||
       (e = cudaMalloc(&P->dstep, sizeof(unsigned long long))) != cudaSuccess ||
-      (e = cudaMalloc(&P->stats_d, sizeof(Stats))) != cudaSuccess)
+      (e = cudaMalloc(&P->stats_d, sizeof(Stats))) != cudaSuccess ||
+      (e = cudaMalloc(&P->ew_ctr, 6 * sizeof(unsigned))) != cudaSuccess ||
+      (e = cudaMemset(P->ew_ctr, 0, 6 * sizeof(unsigned))) != cudaSuccess)
     return bail(fail(WAVE_ERR_ALLOC, "cudaMalloc: %s", cudaGetErrorString(e)));
   if ((e = cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking)) != cudaSuccess ||
       (e = cudaStreamCreateWithFlags(&P->cap, cudaStreamNonBlocking)) != cudaSuccess ||
@@ -1534,6 +1630,14 @@ void wave_plan_destroy(wave_plan* P) {
   if (P->prog_d) cudaFree(P->prog_d);
   if (P->dstep) cudaFree(P->dstep);
   if (P->stats_d) cudaFree(P->stats_d);
+  if (P->ew_ctr) cudaFree(P->ew_ctr);
+  if (P->ew_dbg) {
+    unsigned long long h[6];
+    cudaMemcpy(h, P->ew_dbg, sizeof h, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[ew] during interior: %llu units, %llu planes, %.3f us/plane; mop-up: %llu units, %llu planes, %.3f us/plane\n",
+            h[4], h[1], h[1] ? h[0] * 1e-3 / h[1] : 0.0, h[5], h[3], h[3] ? h[2] * 1e-3 / h[3] : 0.0);
+    cudaFree(P->ew_dbg);
+  }
   if (P->ddone) cudaFree(P->ddone);
   if (P->inc_d) cudaFree(P->inc_d);
   if (P->wl_d) cudaFree(P->wl_d);
@@ -2126,7 +2230,7 @@ float wave_get_dt(const wave_plan* P) { return P ? P->dt : 0.f; }
 // measurement kind of a kernel (the fused launch is the interior kind: it is
 // the dominant kernel and covers every point)
 static int kk_of(int ki) {
-  return ki == KI_FUSED ? WAVE_KK_INTERIOR
+  return (ki == KI_FUSED || ki == KI_EW) ? WAVE_KK_INTERIOR
          : (ki == KI_WALLX_E || ki == KI_SEAM) ? WAVE_KK_XWALLS
          : ki == KI_WALLY_E ? WAVE_KK_YWALLS : ki;
 }
@@ -2141,6 +2245,14 @@ static int64_t region_points(const std::vector<Launch>& Ls, int kind) {
         const int64_t rows = L.ki == KI_SEAM ? (int64_t)(g.y1 - g.y0 - 1) : (int64_t)(g.y1 - g.y0);
         n += (int64_t)(g.x1 - g.x0) * rows * (g.z1 - g.z0);
       }
+  // embedded walls: the wall points are computed by the interior launch
+  if (kind == WAVE_KK_INTERIOR)
+    for (const Launch& L : Ls)
+      if (L.ki == KI_EW)
+        for (int r = 0; r < L.p.ew.nreg; ++r) {
+          const Region& g = L.p.ew.reg[r];
+          n += (int64_t)(g.x1 - g.x0) * (g.y1 - g.y0) * (g.z1 - g.z0);
+        }
   return n;
 }
 

@@ -399,7 +399,7 @@ for name in ("RAGGED", "C1"):
 @pytest.mark.parametrize("env", [
     {"WAVE25_INNER_TILE": "128x16x1"}, {"WAVE25_INNER_TILE": "64x16x1"},
     {"WAVE25_INNER_TILE": "128x8x1"}, {"WAVE25_INNER_TILE": "248x8x1"}, {"WAVE25_INNER_TILE": "224x8x1"},
-    {"WAVE25_INNER_TILE": "248x8x2"}, {"WAVE25_INNER_TILE": "256x8x1r"},
+    {"WAVE25_INNER_TILE": "248x8x2"}, {"WAVE25_INNER_TILE": "248x8x2r"}, {"WAVE25_INNER_TILE": "256x8x1r"},
     {"WAVE25_INNER_TILE": "248x8x1rc2"}, {"WAVE25_INNER_TILE": "248x8x1rc4"},
     {"WAVE25_FASTDIV": "0"}, {"WAVE25_NO_ORIGIN": "1"}, {"WAVE25_XINTER": "0"},
     {"WAVE25_WALLX_TILE": "x24c16x128x1rg"}, {"WAVE25_WALLY_TILE": "y128x16x1rg"},
@@ -415,7 +415,11 @@ for name in ("RAGGED", "C1"):
     {"WAVE25_WALLY_TILE": "y64x8x1m3"}, {"WAVE25_XFUSE": "1"},
     {"WAVE25_FUSED": "1"}, {"WAVE25_FORK": "0", "WAVE25_PF": "0"}, {"WAVE25_CZ": "7"},
     {"WAVE25_ORDER": "-3"}, {"WAVE25_ORDER": "2"}, {"WAVE25_MIX": "1"}, {"WAVE25_MIX": "2"}, {"WAVE25_SIDE2": "0"}, {"WAVE25_WALL_CZ": "114"},
-])
+    # embedded wall warps: default pacing, 1-plane units, every
+    # unit claimed at once, every unit left to the last wave's mop-up
+    {"WAVE25_EW": "1"}, {"WAVE25_EW": "1", "WAVE25_EW_CZ": "1"}, {"WAVE25_EW": "1", "WAVE25_EW_CZ": "5"},
+    {"WAVE25_EW": "1", "WAVE25_EW_REM": "0"}, {"WAVE25_EW": "1", "WAVE25_EW_REM": "1000000"},
+], ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()))
 def test_kernel_variants_bitwise(env):
     # (WAVE25_FASTDIV=0: IEEE divisions instead of the verified table
     # reciprocal -- bitwise the same by the setup check, R9)
