@@ -69,6 +69,12 @@ constexpr int SP = 3;           // u_prev/vdt2 ring stages of the TB2 kernel (di
 #ifndef W25_PACKED
 #define W25_PACKED 1            // fp32 Laplacian on packed pairs (FFMA2); -DW25_PACKED=0 for the scalar A/B build
 #endif
+#ifndef W25_PACK_WALLY
+#define W25_PACK_WALLY 0        // y-wall Laplacian on packed pairs too (A/B build: -DW25_PACK_WALLY=1)
+#endif
+#ifndef W25_PACK_WALLX
+#define W25_PACK_WALLX 0        // x-wall Laplacian on packed pairs (A/B build: -DW25_PACK_WALLX=1)
+#endif
 #ifndef W25_SP_MAX
 #define W25_SP_MAX 4            // deepest u_prev/vdt2 ring k_stream may use (A/B builds: -DW25_SP_MAX=3)
 #endif
@@ -217,9 +223,11 @@ struct StreamCfg {
   static constexpr int E_STAGE = ETA ? (EW * (TY + 2) + 31) / 32 * 32 : 0;  // floats (stages 128-B aligned)
   // u_prev / vdt2 ring depth: as deep as shared memory allows (3..W25_SP_MAX
   // stages), so more of those two streams is in flight per SM
+  // (MINB CTAs per SM share its 228 KB, 1 KB reserved per CTA, ~2 KB static)
+  static constexpr int BUDGET = MINB > 1 ? (233472 / MINB - 1024 - 2048) : W25_SMEM_BUDGET;
   static constexpr int fits_(int n) {
     return (SWZ_ ? 1024 : 0) + (SU * U_STAGE + 2 * n * P_STAGE) * (int)sizeof(T) + n * E_STAGE * 4 +
-               2 * (SU + n) * 8 + (EWB ? EWB + 128 : 0) + 4 * (W25_MAX_W + 2) * (int)sizeof(T) <= W25_SMEM_BUDGET;
+               2 * (SU + n) * 8 + (EWB ? EWB + 128 : 0) + 4 * (W25_MAX_W + 2) * (int)sizeof(T) <= BUDGET;
   }
   static constexpr int SPN = (W25_SP_MAX >= 5 && fits_(5)) ? 5 : (W25_SP_MAX >= 4 && fits_(4)) ? 4 : 3;
   static constexpr int E_OFF = (SU * U_STAGE + 2 * SPN * P_STAGE) * (int)sizeof(T);    // bytes (eta ring)
@@ -239,7 +247,7 @@ struct StreamCfg {
   static_assert((U_HALF * sizeof(T)) % 128 == 0 && (P_STAGE * sizeof(T)) % 128 == 0 && (E_STAGE * 4) % 128 == 0,
                 "TMA smem alignment");
   static_assert(NH == 1 || (CW == TX && TX % 8 == 0 && (HW / NV) % LXW == 0), "half tiles must be warp-aligned");
-  static_assert(RA == 0 || (MINB == 1 && NWC % 4 == 0 && RA % 8 == 0 &&
+  static_assert(RA == 0 || (MINB >= 1 && NWC % 4 == 0 && RA % 8 == 0 &&
                             NWC / 4 * RA + 24 <= (NWC / 4 + 1) * MAXR), "register reallocation budget");
 };
 
@@ -1198,7 +1206,8 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
       T L[TYT][NV];
       // fp32: the 25-point sum on packed pairs of x-points (FMUL2/FADD2/FFMA2,
       // bitwise the scalar chain below element by element, half the issue slots)
-      constexpr bool PK = sizeof(T) == 4 && W25_PACKED && INN;   // (walls: scalar, no spills)
+      constexpr bool PK = sizeof(T) == 4 && W25_PACKED &&
+                          (INN || (W25_PACK_WALLY && MODE == MODE_WALLY) || (W25_PACK_WALLX && MODE == MODE_WALLX));
       if (PK && MODE != MODE_NULL) {
         f2_t L2[TYT][2];
         auto pr = [&](const V& v, int h) -> f2_t {

@@ -98,6 +98,9 @@ static const KInfo* inner_variants(int* n) {
       // registers + the producer warpgroup at 24
       kinfo<248, 248, 8, 2, MODE_INNER, 1, 232>("248x8x2r"),
       kinfo<248, 248, 8, 1, MODE_INNER, 1, 104>("248x8x1r104"),   // consumers at 104 registers (A/B)
+      // two CTAs per SM (each a producer warpgroup at 24 + 8 consumer warps at 104 registers)
+      kinfo<128, 128, 8, 1, MODE_INNER, 2, 104>("128x8x1r2"),
+      kinfo<128, 124, 8, 1, MODE_INNER, 2, 104>("c124x8x1r2"),
       kinfo<248, 248, 4, 1, MODE_INNER, 1>("248x4x1"),
       kinfo<248, 248, 8, 2, MODE_NULL, 1>("null248x8x2"),
       kinfo<224, 224, 4, 1, MODE_INNER, 1>("224x4x1"),
@@ -114,6 +117,7 @@ static const KInfo* wallx_variants(int* n) {
   static const KInfo v[] = {
       kinfo<24, 16, 128, 1, MODE_WALLX, 1, 112>("x24c16x128x1r"),
       kinfo<24, 16, 128, 1, MODE_WALL, 1, 112>("x24c16x128x1rg"),     // generic wall body (A/B)
+      kinfo<24, 16, 64, 1, MODE_WALLX, 2, 104>("x24c16x64x1r2"),      // two CTAs per SM
       kinfo<24, 16, 32, 1, MODE_WALL>("x24c16x32x1"),
       kinfo<28, 16, 32, 1, MODE_WALL>("x28c16x32x1"),
       kinfo<24, 16, 64, 1, MODE_WALL, 1, 232>("x24c16x64x1r"),
@@ -135,6 +139,7 @@ static const KInfo* wally_variants(int* n) {
   static const KInfo v[] = {
       kinfo<128, 128, 16, 1, MODE_WALLY, 1, 112>("y128x16x1r"),
       kinfo<128, 128, 16, 1, MODE_WALL, 1, 112>("y128x16x1rg"),      // generic wall body (A/B)
+      kinfo<128, 128, 8, 1, MODE_WALLY, 2, 104>("y128x8x1r2"),        // two CTAs per SM
       kinfo<64, 64, 8, 1, MODE_WALL, 3>("y64x8x1m3"),
       kinfo<248, 248, 8, 1, MODE_WALL, 1, 112>("y248x8x1r"),
       kinfo<64, 64, 16, 1, MODE_WALL, 2>("y64x16x1m2"),
