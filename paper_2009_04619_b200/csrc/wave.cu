@@ -222,10 +222,30 @@ static void init_kernels() {
   g_k[1][KI_EW] = g_k[1][KI_EWALL] = g_k[1][KI_INNER];   // (fp32 only)
   done = true;
 }
-#define KTX(ki) (g_k[P->prec][ki].tx)
-#define KCW(ki) (g_k[P->prec][ki].cw)
-#define KTY(ki) (g_k[P->prec][ki].ty)
-#define KCL(ki) (g_k[P->prec][ki].cl)
+#define KTX(ki) (P->kt[ki].tx)
+#define KCW(ki) (P->kt[ki].cw)
+#define KTY(ki) (P->kt[ki].ty)
+#define KCL(ki) (P->kt[ki].cl)
+
+// the fp32 interior tile per geometry (unless WAVE25_INNER_TILE names one):
+// the width among 248 / 240 (u boxes of 256 / 248 <= the TMA box limit)
+// whose tiles cover the inner row with the fewest idle lanes, 248 on a tie
+// (C3: 992 = 4 x 248; C2: 480 = 2 x 240 -- 1.6 % faster than 2 x 248 there)
+static KInfo pick_inner(const wave_desc& d, int prec) {
+  if (prec != 0 || getenv("WAVE25_INNER_TILE")) return g_k[prec][KI_INNER];
+  const int64_t W = d.nx - 2 * (int64_t)d.pml_width;
+  if (W <= 0) return g_k[0][KI_INNER];
+  int n = 0;
+  const KInfo* v = inner_variants(&n);
+  const KInfo* best = &g_k[0][KI_INNER];
+  int64_t bw = (W + best->cw - 1) / best->cw * best->cw;
+  for (int i = 0; i < n; ++i)
+    if (!strcmp(v[i].name, "240x8x1r")) {
+      const int64_t c = (W + v[i].cw - 1) / v[i].cw * v[i].cw;
+      if (c < bw) { best = &v[i]; bw = c; }
+    }
+  return *best;
+}
 
 static constexpr double W8[5] = {-205.0 / 72.0, 8.0 / 5.0, -1.0 / 5.0, 8.0 / 315.0, -1.0 / 560.0};
 static constexpr int MAX_W = W25_MAX_W;
@@ -301,6 +321,7 @@ struct wave_plan {
   unsigned long long* dstep = nullptr;
   Stats* stats_d = nullptr;
   // launch plans
+  KInfo kt[KI_N];                    // this plan's kernel per kind (g_k, the interior tile chosen per geometry)
   Maps maps[KI_N];
   int occ[KI_N] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
   bool fused = false;                // WAVE25_FUSED=1: one launch, per-warp paths (measured slower)
@@ -573,9 +594,9 @@ static void make_constants(const wave_desc& d, float dt, Coef* k, std::vector<fl
 // ---------------------------------------------------------------------------
 // launch planning
 // ---------------------------------------------------------------------------
-static void* kernel_ptr(const wave_plan* P, int ki) { return g_k[P->prec][ki].fn; }
-static int kernel_threads(const wave_plan* P, int ki) { return g_k[P->prec][ki].nt; }
-static size_t kernel_smem(const wave_plan* P, int ki) { return g_k[P->prec][ki].smem(P->d.pml_width); }
+static void* kernel_ptr(const wave_plan* P, int ki) { return P->kt[ki].fn; }
+static int kernel_threads(const wave_plan* P, int ki) { return P->kt[ki].nt; }
+static size_t kernel_smem(const wave_plan* P, int ki) { return P->kt[ki].smem(P->d.pml_width); }
 
 // z-chunk length minimising (waves x (chunk + warm-up)) for ncol columns over nz planes
 static int choose_cz(int64_t ncol, int nz, int resident, double warm = 4.0, int maxcz = 1 << 30) {
@@ -725,7 +746,7 @@ static wave_status build_launches(wave_plan* P) {
   // the interior tile rows they border
   P->mix_ok = false;
   if (P->mix && P->prec == 0 && !P->eta_on && !P->fused && !P->xfuse && P->xwall_extra == 0 && w > 0 &&
-      g_k[0][KI_INNER].fn == mix_inner().fn && g_k[0][KI_WALLX].fn == mix_wallx().fn) {
+      P->kt[KI_INNER].fn == mix_inner().fn && P->kt[KI_WALLX].fn == mix_wallx().fn) {
     Launch* Li = nullptr;
     Launch* Lx = nullptr;
     for (Launch& L : P->launches[0]) {
@@ -756,7 +777,7 @@ static wave_status build_launches(wave_plan* P) {
         for (int r = 0; r < 2; ++r)
           for (int t = 0; t < ncw; ++t) {
             const int ymid = pw.reg[r].y0 + t * g_k[0][KI_WALLX].ty + g_k[0][KI_WALLX].ty / 2;
-            const int row = std::max(0, std::min(gi.nty - 1, (ymid - gi.y0) / g_k[0][KI_INNER].ty));
+            const int row = std::max(0, std::min(gi.nty - 1, (ymid - gi.y0) / P->kt[KI_INNER].ty));
             after[row].push_back(-(1 + r * ncw + t));
           }
         std::vector<int> seq;
@@ -1511,11 +1532,13 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, P->dev);
   if (get_encoder() != WAVE_OK) return bail(WAVE_ERR_CUDA);
   init_kernels();
+  for (int ki = 0; ki < KI_N; ++ki) P->kt[ki] = g_k[P->prec][ki];
+  P->kt[KI_INNER] = pick_inner(P->d, P->prec);
   {
     // load every kernel now (lazy module loading can need an idle device,
     // which never comes while a peer-wait kernel spins)
     cudaFuncAttributes fa;
-    for (int ki = 0; ki < KI_N; ++ki) cudaFuncGetAttributes(&fa, g_k[P->prec][ki].fn);
+    for (int ki = 0; ki < KI_N; ++ki) cudaFuncGetAttributes(&fa, P->kt[ki].fn);
     const void* aux[] = {(const void*)k_naive<float>, (const void*)k_source<float>, (const void*)k_vdt2<float>,
                          (const void*)k_inc<float>, (const void*)k_stats<float>, (const void*)k_naive<double>,
                          (const void*)k_source<double>, (const void*)k_vdt2<double>, (const void*)k_inc<double>,
@@ -1715,7 +1738,7 @@ static wave_status encode_buffer(wave_plan* P, int b) {
     // cluster kernels load the u window as (2R)-row boxes (multicast halves)
     const uint32_t UH = KCL(ki) > 1 ? 2 * R : TY + 2 * R;
     CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, UH, f64, -1,
-                  g_k[P->prec][ki].swz));
+                  P->kt[ki].swz));
     CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY, f64,
                   centre_promo(P, ki, CW)));
   }
