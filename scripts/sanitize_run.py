@@ -1,7 +1,7 @@
 """Small end-to-end runs for compute-sanitizer (development aid): every kernel
 family (stream / naive / tb2 / pair), fp32 and fp64, stored eta, the paper-shape
 ablation kernels, graph replay and the slab split path, on C1 / RAGGED-size
-grids."""
+grids; the round-2 variants (embedded wall warps, seams, tile choices) on C1."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -31,6 +31,16 @@ for name, kw in cases:
     run(s, "stream", "fp64")
     run(s, "naive", "fp64")
     run(s, "stream", eta=True)
+# round-2 variants on C1 (64^3, w = 16): embedded wall warps (several pacing
+# settings, incl. 1-plane units and an all-mop-up run), seam x walls, the 248
+# tile (C1 picks 240 by default), two CTAs per SM
+for env in ({"WAVE25_EW": "1"}, {"WAVE25_EW": "1", "WAVE25_EW_CZ": "1"}, {"WAVE25_EW": "1", "WAVE25_EW_REM": "1000000"},
+            {"WAVE25_SEAM": "1"}, {"WAVE25_INNER_TILE": "248x8x1r"}, {"WAVE25_INNER_TILE": "128x8x1r2"},
+            {"WAVE25_WALLX_TILE": "x24c16x64x1r2", "WAVE25_WALLY_TILE": "y128x8x1r2"}):
+    os.environ.update(env)
+    run(synth.scenario("C1"), "stream")
+    for k in env:
+        del os.environ[k]
 if os.environ.get("WAVE25_ABLATION"):
     run(synth.scenario("RAGGED"), "stream")
 # slab split path
