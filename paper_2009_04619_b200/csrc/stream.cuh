@@ -125,6 +125,8 @@ struct StreamParams {
   int pair_pk;                  // step 1 publishes its progress every pair_pk planes (and at the end)
   int64_t pair_dbg_off;         // timeline records (pair_dbg & 8) at prog + this, 6 u64 per block
   int64_t pair_ticket;          // prog[pair_ticket]: next work unit (zeroed with the counters)
+  int st_keep;                  // u_next stored with the default (evict-normal) policy instead of
+                                // streaming (.cs) stores: the next step re-reads it soon (A/B)
   int inter2;                   // 2 equal regions interleaved block by block (the two x walls: the
                                 // right wall of row y and the left wall of row y+1 share a line)
   // stored eta through the u_prev/vdt2 ring (MODE_WALL_ETA): [nz][ny][pitch]
@@ -1471,7 +1473,7 @@ stream_body(const CUtensorMap& tm_u,    // u^n, box (HW+8, TY+8, 1)
         }
       }
       if (full) {
-        if (PAIR && role == 1) {
+        if ((PAIR && role == 1) || P.st_keep) {
           // u^{n+1} is re-read from L2 by the step-2 blocks: normal (not evict-first) stores
 #pragma unroll
           for (int r = 0; r < TYT; ++r) *reinterpret_cast<V*>(optr + r * P.pitch) = res[r];

@@ -352,6 +352,8 @@ struct wave_plan {
   bool seam_on = false;              // WAVE25_SEAM=1: the x walls as seams (measured slower; A/B)
   bool fastdiv = false;              // table division verified bitwise for this plan (check_fastdiv)
   bool walls_last = false;           // WAVE25_WALLS_LAST: enqueue the wall kernels after the interior
+  bool walls_alt = false;            // WAVE25_WALLS_ALT: walls last / first in the two steps of a graph
+  bool wall_keep = false;            // WAVE25_WALL_STKEEP: wall u_next stores evict-normal
   int mix = 0;                       // WAVE25_MIX=1/2: interior + x walls as one grid (k_mix, §5i; measured slower)
   bool mix_ok = false;               // geometry / kernel choice supports k_mix (set by build_launches)
   int* mix_seq_d = nullptr;          // k_mix chunk sequence (device)
@@ -926,6 +928,7 @@ static void add_regions(wave_plan* P, int ki, const std::vector<std::array<int, 
   p.pf = (is_wall(ki) && P->wall_pf >= 0) ? P->wall_pf : P->pf;
   p.order = P->order;
   p.upol = P->upol;
+  p.st_keep = (is_wall(ki) && P->wall_keep) ? 1 : 0;
   int blk = 0;
   auto flush = [&]() {
     if (p.nreg == 0) return;
@@ -1230,6 +1233,18 @@ static wave_status capture(wave_plan* P, cudaGraphExec_t* out, wave_status (*bod
 }
 
 static wave_status two_single_steps(wave_plan* P, int cur, int prv) {
+  if (P->walls_alt) {
+    // walls after the interior in the first step, before it in the second: the
+    // two wall phases are adjacent in time, so the second reads the wall data
+    // the first just wrote / read from L2 (A/B)
+    const bool keep = P->walls_last;
+    P->walls_last = true;
+    wave_status st = enqueue_step(P, cur, prv, P->cap);
+    P->walls_last = false;
+    if (st == WAVE_OK) st = enqueue_step(P, prv, cur, P->cap);
+    P->walls_last = keep;
+    return st;
+  }
   CKST(enqueue_step(P, cur, prv, P->cap));
   return enqueue_step(P, prv, cur, P->cap);
 }
@@ -1565,6 +1580,8 @@ wave_status wave_plan_create(const wave_desc* desc, wave_plan** out) {
   if (const char* e = getenv("WAVE25_PEER_TIMEOUT_S")) P->peer_timeout_s = std::max(1e-3, atof(e));
   if (const char* e = getenv("WAVE25_XWALL_EXTRA")) P->xwall_extra = std::max(0, atoi(e));
   if (const char* e = getenv("WAVE25_WALLS_LAST")) P->walls_last = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_WALLS_ALT")) P->walls_alt = atoi(e) != 0;
+  if (const char* e = getenv("WAVE25_WALL_STKEEP")) P->wall_keep = atoi(e) != 0;
   if (const char* e = getenv("WAVE25_MIX")) P->mix = atoi(e);
   if (const char* e = getenv("WAVE25_WALL_PF")) P->wall_pf = atoi(e);
   if (const char* e = getenv("WAVE25_GMAPS")) P->gmaps = atoi(e) != 0;
