@@ -140,6 +140,7 @@ static const KInfo* wally_variants(int* n) {
       kinfo<128, 128, 16, 1, MODE_WALLY, 1, 112>("y128x16x1r"),
       kinfo<128, 128, 16, 1, MODE_WALL, 1, 112>("y128x16x1rg"),      // generic wall body (A/B)
       kinfo<128, 128, 8, 1, MODE_WALLY, 2, 104>("y128x8x1r2"),        // two CTAs per SM
+      kinfo<248, 248, 8, 1, MODE_WALLY, 1, 112>("y248x8x1ry"),         // the interior's tile shape
       kinfo<64, 64, 8, 1, MODE_WALL, 3>("y64x8x1m3"),
       kinfo<248, 248, 8, 1, MODE_WALL, 1, 112>("y248x8x1r"),
       kinfo<64, 64, 16, 1, MODE_WALL, 2>("y64x16x1m2"),

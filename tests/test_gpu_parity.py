@@ -402,7 +402,8 @@ for name in ("RAGGED", "C1"):
     {"WAVE25_INNER_TILE": "248x8x2"}, {"WAVE25_INNER_TILE": "248x8x2r"}, {"WAVE25_INNER_TILE": "256x8x1r"},
     {"WAVE25_INNER_TILE": "248x8x1rc2"}, {"WAVE25_INNER_TILE": "248x8x1rc4"},
     {"WAVE25_INNER_TILE": "248x8x1r"}, {"WAVE25_INNER_TILE": "240x8x1r"}, {"WAVE25_INNER_TILE": "248x8x1r104"}, {"WAVE25_INNER_TILE": "128x8x1r2"}, {"WAVE25_INNER_TILE": "c124x8x1r2"},
-    {"WAVE25_WALLX_TILE": "x24c16x64x1r2"}, {"WAVE25_WALLY_TILE": "y128x8x1r2"},
+    {"WAVE25_WALLX_TILE": "x24c16x64x1r2"}, {"WAVE25_WALLY_TILE": "y128x8x1r2"}, {"WAVE25_WALLY_TILE": "y248x8x1ry"},
+    {"WAVE25_WALLS_ALT": "1", "WAVE25_WALL_STKEEP": "1"},
     {"WAVE25_FASTDIV": "0"}, {"WAVE25_NO_ORIGIN": "1"}, {"WAVE25_XINTER": "0"},
     {"WAVE25_WALLX_TILE": "x24c16x128x1rg"}, {"WAVE25_WALLY_TILE": "y128x16x1rg"},
     {"WAVE25_SEAM": "1"}, {"WAVE25_SEAM": "1", "WAVE25_NO_SEAM": "1"},
