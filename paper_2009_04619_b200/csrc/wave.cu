@@ -201,8 +201,17 @@ static void init_kernels() {
     g_k[1][KI_WALLX] = pick(dx, 2, "WAVE25_DWALLX_TILE");
     g_k[1][KI_WALLY] = pick(dy, 2, "WAVE25_DWALLY_TILE");
   }
-  g_k[0][KI_WALLX_E] = kinfo<24, 16, 32, 1, MODE_WALL_ETA, 2>("ex24c16x32x1");
-  g_k[0][KI_WALLY_E] = kinfo<64, 64, 8, 1, MODE_WALL_ETA, 3>("ey64x8x1m3");
+  {
+    // stored-eta walls; the producer-warpgroup shapes of the
+    // profile-eta walls as A/B variants
+    static const KInfo ex[] = {kinfo<24, 16, 32, 1, MODE_WALL_ETA, 2>("ex24c16x32x1"),
+                               kinfo<24, 16, 64, 1, MODE_WALL_ETA, 1, 112>("ex24c16x64x1r")};
+    static const KInfo ey[] = {kinfo<64, 64, 8, 1, MODE_WALL_ETA, 3>("ey64x8x1m3"),
+                               kinfo<128, 128, 16, 1, MODE_WALL_ETA, 1, 112>("ey128x16x1r"),
+                               kinfo<128, 128, 8, 1, MODE_WALL_ETA, 1, 112>("ey128x8x1r")};
+    g_k[0][KI_WALLX_E] = pick(ex, 2, "WAVE25_EWALLX_TILE");
+    g_k[0][KI_WALLY_E] = pick(ey, 3, "WAVE25_EWALLY_TILE");
+  }
   g_k[1][KI_WALLX_E] = kinfo<24, 16, 32, 1, MODE_WALL_ETA, 1, 0, double>("edx24c16x32x1");
   g_k[1][KI_WALLY_E] = kinfo<32, 32, 8, 1, MODE_WALL_ETA, 3, 0, double>("edy32x8x1m3");
   g_k[0][KI_PAIR] = kinfo<248, 248, 8, 1, MODE_INNER, 1, 112, float, 1>("pair248x8x1r");
