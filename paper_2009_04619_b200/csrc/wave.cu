@@ -202,12 +202,13 @@ static void init_kernels() {
     g_k[1][KI_WALLY] = pick(dy, 2, "WAVE25_DWALLY_TILE");
   }
   {
-    // stored-eta walls; the producer-warpgroup shapes of the
-    // profile-eta walls as A/B variants
-    static const KInfo ex[] = {kinfo<24, 16, 32, 1, MODE_WALL_ETA, 2>("ex24c16x32x1"),
-                               kinfo<24, 16, 64, 1, MODE_WALL_ETA, 1, 112>("ex24c16x64x1r")};
-    static const KInfo ey[] = {kinfo<64, 64, 8, 1, MODE_WALL_ETA, 3>("ey64x8x1m3"),
-                               kinfo<128, 128, 16, 1, MODE_WALL_ETA, 1, 112>("ey128x16x1r"),
+    // stored-eta walls: producer-warpgroup shapes (x walls
+    // 16 x 64, y walls + caps 128 x 16; C3 serialized 0.355 -> 0.333 and
+    // 0.413 -> 0.335 ms/step, profiles/eta_tiles_r02dd.txt), older shapes as A/B
+    static const KInfo ex[] = {kinfo<24, 16, 64, 1, MODE_WALL_ETA, 1, 112>("ex24c16x64x1r"),
+                               kinfo<24, 16, 32, 1, MODE_WALL_ETA, 2>("ex24c16x32x1")};
+    static const KInfo ey[] = {kinfo<128, 128, 16, 1, MODE_WALL_ETA, 1, 112>("ey128x16x1r"),
+                               kinfo<64, 64, 8, 1, MODE_WALL_ETA, 3>("ey64x8x1m3"),
                                kinfo<128, 128, 8, 1, MODE_WALL_ETA, 1, 112>("ey128x8x1r")};
     g_k[0][KI_WALLX_E] = pick(ex, 2, "WAVE25_EWALLX_TILE");
     g_k[0][KI_WALLY_E] = pick(ey, 3, "WAVE25_EWALLY_TILE");

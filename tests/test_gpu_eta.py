@@ -141,3 +141,40 @@ def test_stored_eta_tb2_falls_back_bitwise():
     a, _, spl_a = run_gpu(s, 10, eta, u0, kernel="stream")
     b, _, spl_b = run_gpu(s, 10, eta, u0, kernel="tb2")
     assert spl_b == 1 and np.array_equal(a, b)
+
+
+ETA_VARIANT_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import numpy as np, synth
+from test_gpu_eta import eta_field
+from paper_2009_04619_b200.wave import WavePlan
+for name in ("RAGGED", "C1"):
+    s = synth.scenario(name)
+    sh = (s.nz, s.ny, s.nx)
+    p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+    p.set_eta(eta_field(s, 5))
+    p.set_velocity(synth.velocity(s))
+    p.set_source(*s.source, synth.wavelet_for(s, 9))
+    p.set_state(synth.random_state(sh, 43), synth.random_state(sh, 44))
+    p.step(9)
+    print(name, hashlib.sha256(p.read(0).cpu().numpy().tobytes()).hexdigest())
+    p.close()
+"""
+
+
+@pytest.mark.parametrize("env", [{"WAVE25_EWALLX_TILE": "ex24c16x32x1"}, {"WAVE25_EWALLY_TILE": "ey64x8x1m3"},
+                                 {"WAVE25_EWALLY_TILE": "ey128x8x1r"}],
+                         ids=lambda e: ",".join(f"{k[7:]}={v}" for k, v in e.items()))
+def test_eta_wall_variants_bitwise(env):
+    # the stored-eta wall tile variants compute bitwise the default's values
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    base = {k: v for k, v in os.environ.items() if not k.startswith("WAVE25_")}
+    ref = subprocess.run([sys.executable, "-c", ETA_VARIANT_SCRIPT, root], env=base, capture_output=True, text=True,
+                         check=True).stdout
+    got = subprocess.run([sys.executable, "-c", ETA_VARIANT_SCRIPT, root], env={**base, **env}, capture_output=True,
+                         text=True, check=True).stdout
+    assert ref.count("\n") == 2 and got == ref
