@@ -59,8 +59,8 @@ def main():
     prod = re.compile(r"k_stream<248, 248, 8, 1, 0, 1, 112, float, 0, 1>|k_stream<32, 32, 64, 1, 7, 1, 112, float, 0, 1>|"
                       r"k_stream<24, 16, 128, 1, 5, 1, 112, float, 0, 1>|k_stream<128, 128, 16, 1, 6, 1, 112, float, 0, 1>|"
                       r"k_stream<124, 124, 8, 1, 0, 1, 112, double, 0, 1>|k_stream<24, 16, 64, 1, 5, 1, 112, double, 0, 1>|"
-                      r"k_stream<64, 64, 16, 1, 6, 1, 112, double, 0, 1>|k_stream<24, 16, 32, 1, 4, 2, 0, float, 0, 1>|"
-                      r"k_stream<64, 64, 8, 1, 4, 3, 0, float, 0, 1>|k_source<float>|k_peer_wait|k_peer_signal|"
+                      r"k_stream<64, 64, 16, 1, 6, 1, 112, double, 0, 1>|k_stream<24, 16, 64, 1, 4, 1, 112, float, 0, 1>|"
+                      r"k_stream<128, 128, 16, 1, 4, 1, 112, float, 0, 1>|k_source<float>|k_peer_wait|k_peer_signal|"
                       r"k_vdt2<float>|k_inc<float>|k_stats<float>")
     print(f"# SASS summary of {LIB} (cuobjdump -sass / -res-usage), sm_100a")
     print("# kernel | regs stack shared local | total instr | " + " ".join(KEYS))
