@@ -56,7 +56,7 @@ def main():
     dem = dict(zip(names, demangle(names)))
     # HEAD's production instantiations (wave.cu init_kernels defaults): fp32 interior, seam x walls,
     # two-region x walls (non-16 PML widths), y walls; fp64 interior / walls; the stored-eta walls
-    prod = re.compile(r"k_stream<248, 248, 8, 1, 0, 1, 112, float, 0, 1>|k_stream<32, 32, 64, 1, 7, 1, 112, float, 0, 1>|"
+    prod = re.compile(r"k_stream<248, 248, 8, 1, 0, 1, 112, float, 0, 1>|k_stream<240, 240, 8, 1, 0, 1, 112, float, 0, 1>|k_stream<32, 32, 64, 1, 7, 1, 112, float, 0, 1>|"
                       r"k_stream<24, 16, 128, 1, 5, 1, 112, float, 0, 1>|k_stream<128, 128, 16, 1, 6, 1, 112, float, 0, 1>|"
                       r"k_stream<124, 124, 8, 1, 0, 1, 112, double, 0, 1>|k_stream<24, 16, 64, 1, 5, 1, 112, double, 0, 1>|"
                       r"k_stream<64, 64, 16, 1, 6, 1, 112, double, 0, 1>|k_stream<24, 16, 64, 1, 4, 1, 112, float, 0, 1>|"
