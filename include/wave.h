@@ -149,9 +149,10 @@ typedef struct {
     int64_t elem_bytes;   /* 4 (fp32 plans) or 8 (fp64 plans): buffer element size        */
     int64_t origin;       /* elements before the layout's first element: the 128-B line
                              shift, plus one pad row when `seam` is set                   */
-    int64_t seam;         /* 1: the x walls run as seams (both walls of adjacent rows in
-                             one line); the buffers then also end with one
-                             pad row; never written, read only into masked lanes          */
+    int64_t seam;         /* 1: the layout admits the seam x-wall variant (both walls of
+                             adjacent rows in one line; opt-in, measured
+                             slower): one pad row before (in `origin`) and after the
+                             buffers; never written, read only into masked lanes          */
 } wave_layout_info;
 
 /* One region of the paper's 7-region decomposition (PAPER.md L342-356,
