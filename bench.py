@@ -231,6 +231,13 @@ def ncu_traffic(kernel_tag: str):
         return None
 
 
+def kind_roof(bytes_per_step: float, ms_per_step: float, peak: float) -> dict:
+    """Algorithmic GB/s of one kernel kind (its points x bytes per point over
+    its serialized time per step) and its fraction of the roofline peak."""
+    gbs = bytes_per_step / (ms_per_step / 1e3) / 1e9
+    return {"gbs": gbs, "frac": gbs / peak, "ms_per_step": ms_per_step}
+
+
 def roof_probe(torch):
     """3-read / 1-write streaming probe (out = a + b*c) over 2^28 fp32: the
     stencil's exact byte mix with zero halo -- the practical HBM roof."""
@@ -457,6 +464,10 @@ def run_ours(args, rank, world, local):
                 "kernel_ms_per_step": {k: v / max(args.steps, 1) for k, v in kms.items()},
                 "kernel_points_per_step": kpts,
                 "share_of_step": kms["interior"] / max(sum(kms.values()), 1e-9),
+                # every kernel kind's algorithmic GB/s and fraction of the same peak (the walls:
+                # their points x the same bytes per point / their serialized launch time)
+                "per_kind": {k: kind_roof(bpl * kpts[k], kms[k] / max(args.steps, 1), peak)
+                             for k in ("interior", "xwalls", "ywalls") if kpts.get(k) and kms.get(k)},
                 "how": "CUDA events around each launch on the launching stream, profiled pass of K steps right after the first timed run "
                        "(direct launches serialized on that stream, so each event pair times one kernel)"}
         if not args.no_probe:
