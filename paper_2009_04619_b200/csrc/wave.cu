@@ -195,10 +195,11 @@ static void init_kernels() {
   g_k[1][KI_INNER] = kinfo<124, 124, 8, 1, MODE_INNER, 1, 112, double>("d124x8x1r");
   {
     static const KInfo dx[] = {kinfo<24, 16, 64, 1, MODE_WALLX, 1, 112, double>("dx24c16x64x1r"),
-                               kinfo<24, 16, 32, 1, MODE_WALL, 1, 0, double>("dx24c16x32x1")};
+                               kinfo<24, 16, 32, 1, MODE_WALL, 1, 0, double>("dx24c16x32x1"),
+                               kinfo<24, 16, 32, 1, MODE_WALLX, 1, 168, double>("dx24c16x32x1r")};
     static const KInfo dy[] = {kinfo<64, 64, 16, 1, MODE_WALLY, 1, 112, double>("dy64x16x1r"),
                                kinfo<32, 32, 8, 1, MODE_WALL, 3, 0, double>("dy32x8x1m3")};
-    g_k[1][KI_WALLX] = pick(dx, 2, "WAVE25_DWALLX_TILE");
+    g_k[1][KI_WALLX] = pick(dx, 3, "WAVE25_DWALLX_TILE");
     g_k[1][KI_WALLY] = pick(dy, 2, "WAVE25_DWALLY_TILE");
   }
   {

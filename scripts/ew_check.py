@@ -1,6 +1,6 @@
 """Bitwise check of an env variant against the default path on a full-size
 scenario from a random O(1) state (every wall point active), development aid:
-python scripts/ew_check.py C2 8 WAVE25_EW=1 [WAVE25_EW_CZ=16 ...]"""
+python scripts/ew_check.py C2 8 WAVE25_EW=1 [WAVE25_EW_CZ=16 ...]   (CHECK_PREC=fp64: an fp64 plan)"""
 import hashlib
 import os
 import subprocess
@@ -14,12 +14,15 @@ import numpy as np, torch, synth
 from paper_2009_04619_b200.wave import WavePlan
 s = synth.scenario(sys.argv[2]); n = int(sys.argv[3])
 sh = (s.nz, s.ny, s.nx)
-p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max)
+import os
+prec = os.environ.get("CHECK_PREC", "fp32")
+p = WavePlan(s.nx, s.ny, s.nz, s.w, s.h, s.dt, s.eta_max, precision=prec)
 p.set_velocity(synth.velocity(s))
 p.set_source(*s.source, synth.wavelet_for(s, n))
 g = torch.Generator(device="cuda").manual_seed(7)
-um1 = torch.rand(sh, generator=g, device="cuda") - 0.5
-u0 = torch.rand(sh, generator=g, device="cuda") - 0.5
+dt_ = torch.float64 if prec == "fp64" else torch.float32
+um1 = torch.rand(sh, generator=g, device="cuda", dtype=dt_) - 0.5
+u0 = torch.rand(sh, generator=g, device="cuda", dtype=dt_) - 0.5
 p.set_state(um1, u0)
 p.step(n)
 a = p.read(0).cpu().numpy(); b = p.read(1).cpu().numpy()
