@@ -1766,8 +1766,9 @@ static wave_status encode_buffer(wave_plan* P, int b) {
     }
     // cluster kernels load the u window as (2R)-row boxes (multicast halves)
     const uint32_t UH = KCL(ki) > 1 ? 2 * R : TY + 2 * R;
-    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, UH, f64, -1,
-                  P->kt[ki].swz));
+    static const int xupromo = getenv("WAVE25_XWALL_UPROMO") ? atoi(getenv("WAVE25_XWALL_UPROMO")) : -1;  // A/B
+    CKST(encode3d(&P->maps[ki].u[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, TX + 2 * R, UH, f64,
+                  ki == KI_WALLX ? xupromo : -1, P->kt[ki].swz));
     CKST(encode3d(&P->maps[ki].up[b], P->buf[b], P->d.nx, P->d.ny, P->L.planes, pb, plb, CW, TY, f64,
                   centre_promo(P, ki, CW)));
   }
