@@ -1951,6 +1951,9 @@ wave_status wave_set_state(wave_plan* P, const float* uprev, const float* ucur, 
                            P->d.nx * P->esz, P->d.nx * P->esz, P->d.ny * P->d.nz, kind, s));
   }
   CK(cudaMemsetAsync(P->dstep, 0, sizeof(unsigned long long), s));
+  // embedded-wall tickets re-armed too (they self-reset at every launch end; an
+  // aborted launch would otherwise leave them mid-count)
+  if (P->ew_ctr) CK(cudaMemsetAsync(P->ew_ctr, 0, 6 * sizeof(unsigned), s));
   if (P->have_peers) {
     // restart the step-flag protocol from 0 (collective: every rank of the
     // run re-initialises between two barriers) -- otherwise a
